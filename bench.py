@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark: distributed sample sort (SIHSort) of Int64 keys.
+
+Metric (BASELINE.json): sort throughput GB/s of Int64 keys = total key bytes
+sorted across all ranks / 1e9 / seconds per step (reference bench.cpp:74-76, :213).
+Workload (BASELINE config 4): 2^28 uniform-random full-range Int64 keys per GPU from
+the reference bench generator (mt19937_64(seed + 0x9e3779b97f4a7c15*(r+1)),
+bench.cpp:164-173), weak scaling, one rank per GPU, NCCL between GPUs.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one full ak.sihsort (local radix sort, sampling, splitters, refinement,
+NCCL all-to-all-v, P-way merge) of device-resident input into a device output.
+`e2e` = the same through the host-buffer C-ABI entry (H2D + sort + D2H per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sort throughput GB/s (Int64 keys) at 1/2/4/8 B200; % of HBM/NVLink roofline"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--log2n", type=int, default=28, help="keys per GPU = 2^log2n (config 4: 28, config 5: 30)")
+    p.add_argument("--dtype", choices=["int64", "uint64"], default="int64")
+    p.add_argument("--seed", type=int, default=42)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per onesweep launch from the committed ncu --set full summary (or None)."""
+    path = os.path.join(ROOT, "profiles", "onesweep_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch_per_key")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                clk, mx, util = float(parts[0]), float(parts[1]), float(parts[2])
+            except ValueError:
+                continue
+            smax.append(mx)
+            if util > 0:
+                sm.append(clk)
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.lines), "samples_under_load": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def reference_arm(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref: /root/reference/proj compiled in place)
+    over its sim::world with P = N ranks, every host thread in use, bounded per-rank sample."""
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    import paper_2507_16710_b200 as ak
+
+    cores = os.cpu_count() or 1
+    P = world
+    n_sample = 1 << 22  # keys per rank in the CPU sample (bounded: the whole run stays within minutes)
+    dt = np.int64 if args.dtype == "int64" else np.uint64
+    ins = [ak.bench_keys(args.seed, r, n_sample, dt) for r in range(P)]
+    kind = "reference" if oracle.ref_available() else "port"
+    tpr = max(1, cores // P)
+
+    def step():
+        if kind == "reference":
+            oracle.ref_sihsort(ins, threads_per_rank=tpr)
+        else:
+            oracle.sihsort(ins)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(times)
+    gbs = P * n_sample * 8 / 1e9 / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"reference sihsort (sim::world, {P} ranks) of Int64 keys; CPU sample "
+                               f"{n_sample} keys/rank of the 2^{args.log2n}/GPU workload",
+                   "keys_per_rank": n_sample, "ranks": P, "threads_per_rank": tpr},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": tpr * P if kind == "reference" else 1,
+                         "kind": kind, "sample": f"{P} ranks x {n_sample} keys (bench generator, seed {args.seed})"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args):
+    """Reference CPU path on this host, bounded sample, rank 0 / N=1 only."""
+    import numpy as np
+    import oracle
+    import paper_2507_16710_b200 as ak
+
+    cores = os.cpu_count() or 1
+    n = 1 << 24
+    x = ak.bench_keys(args.seed, 0, n, np.int64 if args.dtype == "int64" else np.uint64)
+    kind = "reference" if oracle.ref_available() else "port"
+    run = (lambda: oracle.ref_sihsort([x], threads_per_rank=cores)) if kind == "reference" else \
+        (lambda: oracle.sihsort([x]))
+    run()
+    t = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        run()
+        t.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(t)
+    return {"value": n * 8 / 1e9 / (ms / 1e3), "unit": "GB/s", "cores": cores if kind == "reference" else 1,
+            "kind": kind, "sample": f"sihsort P=1 of {n} bench keys (2^24), mean of 3 after 1 warm-up, "
+                                    f"{ms:.1f} ms/sort"}
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        reference_arm(args, rank, max(world, args.gpus if world == 1 else world))
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2507_16710_b200 as ak
+
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    pg = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+        obj = [ak.NcclComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = ak.NcclComm(obj[0], world, rank, local)
+
+    ex = ak.ExecBackend(local)
+    n = 1 << args.log2n
+    np_dt = np.int64 if args.dtype == "int64" else np.uint64
+    t_dt = torch.int64 if args.dtype == "int64" else torch.uint64
+
+    # inputs: reference generator on the host -> pinned -> HBM (outside the timed region)
+    h_in = torch.empty(n, dtype=t_dt, pin_memory=True)
+    ak.bench_keys(args.seed, rank, n, np_dt, out=h_in.numpy())
+    d_in = h_in.to(dev, non_blocking=False)
+    cap = n if world == 1 else int(1.3 * n) + 4096
+    d_out = torch.empty(cap, dtype=t_dt, device=dev)
+    cfg = ak.SihConfig()
+
+    def barrier():
+        if comm is not None:
+            comm.barrier(ex)
+        torch.cuda.synchronize(dev)
+
+    def step():
+        nonlocal d_out
+        try:
+            return ak.sihsort(d_in, comm, cfg, ex, out=d_out, capacity=d_out.numel())
+        except ak.CapacityError as e:  # raised on every rank consistently; grow and retry
+            d_out = torch.empty(max(e.required, d_out.numel()) + 4096, dtype=t_dt, device=dev)
+            return ak.sihsort(d_in, comm, cfg, ex, out=d_out, capacity=d_out.numel())
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(max(args.warmup, 3)):
+        out, st = step()
+
+    # ---- timed region: device-resident input -> device output ----
+    ex.reset_kernel_time()
+    ex.set_profiling(True)
+    launches0 = ex.kernel_launches()
+    barrier()
+    stream = ex.stream
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        out, st = step()
+    e1.record(stream)
+    barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    gpu_launches = ex.kernel_launches() - launches0
+    ex.set_profiling(False)
+    fam = {k: ex.kernel_time(k) for k in ("onesweep", "hist", "merge", "exchange")}
+    ms = ms_local
+    if comm is not None:
+        ms = comm.allreduce_max([ms_local], ex)[0]
+
+    # ---- e2e: host buffers through the C ABI (H2D + sihsort + D2H each step) ----
+    e2e = None
+    if not args.no_e2e:
+        h_out = torch.empty(d_out.numel(), dtype=t_dt, pin_memory=True)
+        hin_np, hout_np = h_in.numpy(), h_out.numpy()
+        res, _ = ak.sihsort_host(hin_np, comm, cfg, ex, out=hout_np)  # warm-up
+        barrier()
+        k = max(3, min(args.steps, 10))
+        d2h = 0
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
+        for _ in range(k):
+            res, _ = ak.sihsort_host(hin_np, comm, cfg, ex, out=hout_np)
+            d2h = res.size * 8
+        e3.record(stream)
+        barrier()
+        e2e_ms = e2.elapsed_time(e3) / k
+        if comm is not None:
+            e2e_ms = comm.allreduce_max([e2e_ms], ex)[0]
+        e2e = {"value": world * n * 8 / 1e9 / (e2e_ms / 1e3), "unit": "GB/s", "h2d_bytes_per_step": n * 8,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+    clocks = sampler.stop()
+
+    # correctness guard on the last output (sortedness of this rank's slice)
+    o = out.view(torch.int64) if t_dt == torch.int64 else (out.view(torch.int64) ^ (-(1 << 63)))
+    sorted_ok = bool((o[1:] >= o[:-1]).all()) if o.numel() > 1 else True
+
+    if rank != 0:
+        if pg is not None:
+            pg.destroy_process_group()
+        return
+
+    peak, peak_kind = measured_peaks()
+    os_ms, os_cnt = fam["onesweep"]
+    avg_launch_ms = os_ms / max(os_cnt, 1)
+    # onesweep pass: reads + writes every key once: 16 B/key algorithmic
+    alg_bytes = 16 * n
+    achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9 if os_cnt else None
+    tr = ncu_traffic()
+    roofline = {"bound": "hbm", "kernel": "onesweep_kernel (one 8-bit digit pass)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": (tr * n) if tr else None,
+                "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                "avg_launch_ms": avg_launch_ms, "launches": os_cnt}
+    value = world * n * 8 / 1e9 / (ms / 1e3)
+    phases = {k: v[0] / args.steps for k, v in fam.items()}
+    floor_ms = (136 * n) / (peak * 1e9) * 1e3  # local radix sort floor (D=8): 17 passes x 8 B
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"distributed sample sort (SIHSort) of 2^{args.log2n} {args.dtype.capitalize()} "
+                               f"keys per GPU (BASELINE config {'4' if args.log2n == 28 else '5'})",
+                   "keys_per_gpu": n, "global_keys": world * n, "parallelism": f"sihsort over {world} GPU(s)",
+                   "generator": "reference bench.cpp mt19937_64 per-rank seeds", "l2": "inputs > L2 (no flush)",
+                   "sorted_check": sorted_ok},
+        "roofline": roofline,
+        "phases_ms_per_step": phases,
+        "sort_floor_ms": floor_ms,
+        "gpu_launches": gpu_launches,
+        "clocks": clocks,
+    }
+    if world > 1 and fam["exchange"][1]:
+        ex_ms = fam["exchange"][0] / fam["exchange"][1]
+        line["nvlink"] = {"exchange_ms": ex_ms, "bytes_sent_per_gpu": (world - 1) / world * n * 8,
+                          "bus_gbs": (world - 1) / world * n * 8 / 1e9 / (ex_ms / 1e3), "peak_gbs": 770.0}
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args)
+        except Exception as exc:  # the baseline is reported, never the product
+            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference",
+                                    "sample": f"unavailable: {exc}"}
+    print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,437 @@
+// radix_sort.cu -- onesweep radix sort kernels (see radix_sort.cuh).
+#include <type_traits>
+
+#include "radix_sort.cuh"
+
+namespace akb {
+
+namespace {
+
+constexpr int RADIX = 256;
+constexpr std::uint32_t FULL = 0xffffffffu;
+
+template <typename T>
+struct tile_cfg {
+    static constexpr int BLOCK = 384;
+    static constexpr int ITEMS = sizeof(T) == 8 ? 16 : 16;
+    static constexpr int TILE = BLOCK * ITEMS;
+    static constexpr int MIN_BLOCKS = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ std::uint32_t digit_of(T key, int shift, bool desc) {
+    return static_cast<std::uint32_t>((ordered(key, desc) >> shift) & 0xffu);
+}
+
+// Lanes holding the same 8-bit digit, via 8 ballots.
+__device__ __forceinline__ std::uint32_t match_digit(std::uint32_t d) {
+    std::uint32_t m = FULL;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const std::uint32_t bal = __ballot_sync(FULL, bit);
+        m &= bit ? bal : ~bal;
+    }
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// Upfront histogram: one read of the keys, all D digit histograms.
+// PARTS sub-histograms per digit spread same-digit lanes over banks.
+// ---------------------------------------------------------------------------
+template <typename T, int PASSES>
+__global__ void __launch_bounds__(256) hist_kernel(const T* __restrict__ keys, std::uint64_t n,
+                                                   int desc, std::uint64_t* __restrict__ g_hist) {
+    constexpr int PARTS = 4;
+    __shared__ std::uint32_t sh[PASSES * RADIX * PARTS];
+    for (int i = threadIdx.x; i < PASSES * RADIX * PARTS; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int part = threadIdx.x % PARTS;
+    auto count = [&](T k) {
+        const auto o = ordered(k, desc != 0);
+#pragma unroll
+        for (int p = 0; p < PASSES; ++p) {
+            const std::uint32_t d = static_cast<std::uint32_t>((o >> (8 * p)) & 0xffu);
+            atomicAdd(&sh[(p * RADIX + d) * PARTS + part], 1u);
+        }
+    };
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    constexpr int VEC = 16 / sizeof(T);
+    const bool aligned = (reinterpret_cast<std::uintptr_t>(keys) & 15) == 0;
+    std::uint64_t done = 0;
+    if (aligned) {
+        const std::uint64_t nv = n / VEC;
+        const uint4* kv = reinterpret_cast<const uint4*>(keys);
+        std::uint64_t i = tid;
+        for (; i + 3 * stride < nv; i += 4 * stride) {
+            uint4 a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = __ldg(kv + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const T* e = reinterpret_cast<const T*>(&a[u]);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) count(e[v]);
+            }
+        }
+        for (; i < nv; i += stride) {
+            const uint4 a = __ldg(kv + i);
+            const T* e = reinterpret_cast<const T*>(&a);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) count(e[v]);
+        }
+        done = nv * VEC;
+    }
+    for (std::uint64_t i = done + tid; i < n; i += stride) count(keys[i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) {
+        std::uint32_t s = 0;
+#pragma unroll
+        for (int q = 0; q < PARTS; ++q) s += sh[i * PARTS + q];
+        if (s) atomicAdd(reinterpret_cast<unsigned long long*>(g_hist + i),
+                         static_cast<unsigned long long>(s));
+    }
+}
+
+// Exclusive scan of each pass's 256 digit counts -> global digit offsets.
+__global__ void __launch_bounds__(RADIX) hist_scan_kernel(const std::uint64_t* __restrict__ g_hist,
+                                                          std::uint64_t* __restrict__ g_offs) {
+    __shared__ std::uint64_t s_warp[RADIX / 32];
+    const int p = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const std::uint64_t v = g_hist[p * RADIX + t];
+    std::uint64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint64_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    std::uint64_t base = 0;
+    for (int i = 0; i < w; ++i) base += s_warp[i];
+    g_offs[p * RADIX + t] = base + inc - v;
+}
+
+// ---------------------------------------------------------------------------
+// One onesweep digit pass.
+// ---------------------------------------------------------------------------
+template <typename T, typename V, int MODE>
+struct pass_smem {
+    static constexpr int BLOCK = tile_cfg<T>::BLOCK;
+    static constexpr int TILE = tile_cfg<T>::TILE;
+    static constexpr int WARPS = BLOCK / 32;
+    static constexpr bool HAS_KEYS_SMEM = MODE != SORT_LOWMEM;
+    static constexpr bool HAS_VALS = MODE != SORT_KEYS;
+    static constexpr std::size_t keys_off = 0;
+    static constexpr std::size_t keys_bytes = HAS_KEYS_SMEM ? sizeof(T) * TILE : 0;
+    static constexpr std::size_t vals_off = keys_off + keys_bytes;
+    static constexpr std::size_t vals_bytes = HAS_VALS ? sizeof(V) * TILE : 0;
+    static constexpr std::size_t whist_off = (vals_off + vals_bytes + 15) & ~std::size_t(15);
+    static constexpr std::size_t whist_bytes = sizeof(std::uint32_t) * WARPS * RADIX;
+    static constexpr std::size_t gofs_off = whist_off + whist_bytes;
+    static constexpr std::size_t gofs_bytes = sizeof(std::uint64_t) * RADIX;
+    static constexpr std::size_t misc_off = gofs_off + gofs_bytes;
+    static constexpr std::size_t misc_bytes = sizeof(std::uint32_t) * 16;
+    static constexpr std::size_t total = misc_off + misc_bytes;
+};
+
+template <typename T, typename V, int MODE>
+__global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
+    onesweep_kernel(const T* __restrict__ kin, T* __restrict__ kout, const V* __restrict__ vin,
+                    V* __restrict__ vout, std::uint64_t n, int shift, int desc, int pass_index,
+                    const std::uint64_t* __restrict__ goffs, std::uint64_t* lookback,
+                    std::uint32_t* tile_counter, std::uint32_t tag, int write_keys) {
+    using L = pass_smem<T, V, MODE>;
+    constexpr int BLOCK = L::BLOCK;
+    constexpr int ITEMS = tile_cfg<T>::ITEMS;
+    constexpr int TILE = L::TILE;
+    constexpr int WARPS = L::WARPS;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* s_keys = reinterpret_cast<T*>(smem + L::keys_off);
+    V* s_vals = reinterpret_cast<V*>(smem + L::vals_off);
+    std::uint32_t* s_whist = reinterpret_cast<std::uint32_t*>(smem + L::whist_off);
+    std::uint64_t* s_gofs = reinterpret_cast<std::uint64_t*>(smem + L::gofs_off);
+    std::uint32_t* s_misc = reinterpret_cast<std::uint32_t*>(smem + L::misc_off);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool dsc = desc != 0;
+    if (tid == 0) s_misc[0] = atomicAdd(tile_counter, 1u);
+    for (int i = tid; i < WARPS * RADIX; i += BLOCK) s_whist[i] = 0;
+    __syncthreads();
+    const std::uint32_t tile = s_misc[0];
+    const std::uint64_t tile_base = static_cast<std::uint64_t>(tile) * TILE;
+    const std::uint64_t remaining = n - tile_base;
+    const std::uint32_t valid = remaining < TILE ? static_cast<std::uint32_t>(remaining) : TILE;
+    const std::uint64_t wbase = tile_base + static_cast<std::uint64_t>(warp) * 32 * ITEMS;
+
+    // ---- load (warp-striped: item i of lane l is key wbase + 32 i + l) ----
+    T k[ITEMS];
+    V v[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint64_t idx = wbase + i * 32 + lane;
+        const bool ok = idx < n;
+        if constexpr (MODE == SORT_LOWMEM) {
+            if (ok) {
+                const V ix = pass_index == 0 ? static_cast<V>(idx) : vin[idx];
+                v[i] = ix;
+                k[i] = kin[ix];
+            } else {
+                v[i] = V(0);
+                k[i] = T(0);
+            }
+        } else {
+            k[i] = ok ? kin[idx] : T(0);
+            if constexpr (MODE == SORT_PAIRS) v[i] = ok ? vin[idx] : V(0);
+            if constexpr (MODE == SORT_IOTA) v[i] = static_cast<V>(idx);
+        }
+    }
+
+    // ---- warp-level stable ranking ----
+    std::uint32_t rk[ITEMS];
+    std::uint32_t* wh = s_whist + warp * RADIX;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint64_t idx = wbase + i * 32 + lane;
+        const std::uint32_t d = idx < n ? digit_of(k[i], shift, dsc) : 255u;
+        const std::uint32_t peers = match_digit(d);
+        const int leader = __ffs(peers) - 1;
+        const std::uint32_t below = __popc(peers & lanemask_lt());
+        std::uint32_t base = 0;
+        if (lane == leader) {
+            base = wh[d];
+            wh[d] = base + __popc(peers);
+        }
+        base = __shfl_sync(FULL, base, leader);
+        rk[i] = base + below;
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // ---- tile digit totals, warp-exclusive offsets, publish aggregate ----
+    std::uint32_t total = 0;
+    std::uint32_t incl = 0;
+    std::uint64_t* my_lb = lookback + static_cast<std::uint64_t>(tile) * RADIX + tid;
+    const std::uint64_t tagbits = static_cast<std::uint64_t>(tag) << LB_TAG_SHIFT;
+    if (tid < RADIX) {
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+            const std::uint32_t c = s_whist[w * RADIX + tid];
+            s_whist[w * RADIX + tid] = total;
+            total += c;
+        }
+        const std::uint32_t pad = (tid == RADIX - 1) ? (TILE - valid) : 0u;
+        const std::uint64_t mine = total - pad;
+        st_relaxed_u64(my_lb, (tile == 0 ? LB_INC : LB_AGG) | tagbits | mine);
+        incl = total;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_misc[4 + warp] = incl;
+    }
+    __syncthreads();
+    std::uint32_t dstart = 0;
+    if (tid < RADIX) {
+        std::uint32_t wp = 0;
+#pragma unroll
+        for (int w = 0; w < RADIX / 32; ++w)
+            if (w < warp) wp += s_misc[4 + w];
+        dstart = wp + incl - total;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) s_whist[w * RADIX + tid] += dstart;
+    }
+    __syncthreads();
+
+    // ---- stage keys (and payload) in shared memory in digit order ----
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint64_t idx = wbase + i * 32 + lane;
+        const std::uint32_t d = idx < n ? digit_of(k[i], shift, dsc) : 255u;
+        const std::uint32_t pos = s_whist[warp * RADIX + d] + rk[i];
+        if constexpr (L::HAS_KEYS_SMEM) s_keys[pos] = k[i];
+        if constexpr (L::HAS_VALS) s_vals[pos] = v[i];
+        if constexpr (MODE == SORT_LOWMEM) rk[i] = pos;  // reuse: remember digit order position
+        (void)pos;
+    }
+
+    // ---- decoupled look-back for this tile's per-digit exclusive prefix ----
+    if (tid < RADIX) {
+        std::uint64_t excl = 0;
+        if (tile > 0) {
+            std::int64_t p = static_cast<std::int64_t>(tile) - 1;
+            while (true) {
+                const std::uint64_t w = ld_relaxed_u64(lookback + p * RADIX + tid);
+                const std::uint32_t wtag = static_cast<std::uint32_t>(w >> LB_TAG_SHIFT) & LB_TAG_MASK;
+                const std::uint64_t flag = w & (3ull << 62);
+                if (wtag != tag || flag == 0) continue;
+                excl += w & LB_COUNT_MASK;
+                if (flag == LB_INC) break;
+                --p;
+            }
+            const std::uint32_t pad = (tid == RADIX - 1) ? (TILE - valid) : 0u;
+            st_relaxed_u64(my_lb, LB_INC | tagbits | (excl + total - pad));
+        }
+        s_gofs[tid] = goffs[tid] + excl - dstart;
+    }
+    __syncthreads();
+
+    // ---- scatter contiguous digit runs ----
+    if constexpr (MODE == SORT_LOWMEM) {
+        // only the index array moves; the digit of staged slot j is recomputed
+        // from data[index] (L1/L2 hit: just gathered by this tile)
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t j = i * BLOCK + tid;
+            if (j < valid) {
+                const V ix = s_vals[j];
+                const std::uint32_t d = digit_of(kin[ix], shift, dsc);
+                vout[s_gofs[d] + j] = ix;
+            }
+        }
+    } else {
+        std::uint8_t dj[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t j = i * BLOCK + tid;
+            dj[i] = 0;
+            if (j < valid) {
+                const T key = s_keys[j];
+                const std::uint32_t d = digit_of(key, shift, dsc);
+                dj[i] = static_cast<std::uint8_t>(d);
+                if (write_keys) kout[s_gofs[d] + j] = key;
+            }
+        }
+        if constexpr (L::HAS_VALS) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const std::uint32_t j = i * BLOCK + tid;
+                if (j < valid) vout[s_gofs[dj[i]] + j] = s_vals[j];
+            }
+        }
+    }
+}
+
+template <typename T, typename V, int MODE>
+void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n,
+                 int shift, bool desc, int pass_index, const std::uint64_t* goffs,
+                 std::uint32_t* tile_counter, bool write_keys) {
+    using L = pass_smem<T, V, MODE>;
+    static bool configured = false;
+    auto kern = onesweep_kernel<T, V, MODE>;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(L::total)));
+        configured = true;
+    }
+    const std::uint64_t tiles = ceil_div(n, L::TILE);
+    const std::uint32_t tag = ctx_lookback_pass(c, tiles);
+    const int tok = ctx_prof_begin(c, KF_ONESWEEP);
+    kern<<<static_cast<unsigned>(tiles), L::BLOCK, L::total, c->stream>>>(
+        kin, kout, vin, vout, n, shift, desc ? 1 : 0, pass_index, goffs, c->lookback,
+        tile_counter, tag, write_keys ? 1 : 0);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 1;
+}
+
+template <typename T, typename V, int MODE>
+void radix_sort_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, const V* vin, V* vout, V* valt,
+                     std::uint64_t n, bool desc, bool keys_out) {
+    constexpr int PASSES = key_traits<T>::nbits / 8;
+    static_assert(PASSES % 2 == 0, "even pass count keeps the result in the output buffer");
+    if (n == 0) return;
+    // small region: hist | offs | tile counters
+    std::uint64_t* g_hist = static_cast<std::uint64_t*>(c->small);
+    std::uint64_t* g_offs = g_hist + PASSES * RADIX;
+    std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
+    AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
+
+    // upfront histogram (for LOWMEM the keys are the data array itself)
+    {
+        const int blocks = c->sm_count * 4;
+        const int tok = ctx_prof_begin(c, KF_HIST);
+        hist_kernel<T, PASSES><<<blocks, 256, 0, c->stream>>>(kin, n, desc ? 1 : 0, g_hist);
+        AKB_CUDA(cudaGetLastError());
+        ctx_prof_end(c, tok);
+        hist_scan_kernel<<<PASSES, RADIX, 0, c->stream>>>(g_hist, g_offs);
+        AKB_CUDA(cudaGetLastError());
+        c->kernel_launches += 2;
+    }
+
+    if constexpr (MODE == SORT_LOWMEM) {
+        // indices ping-pong valt <-> vout; pass 0 synthesises iota
+        for (int p = 0; p < PASSES; ++p) {
+            V* dst = (p % 2 == 0) ? valt : vout;
+            const V* src = (p % 2 == 0) ? vout : valt;  // unused at p == 0
+            launch_pass<T, V, MODE>(c, kin, nullptr, src, dst, n, 8 * p, desc, p,
+                                    g_offs + p * RADIX, counters + p, false);
+        }
+        return;
+    }
+    // keys: pass p reads src, writes dst; even passes -> kalt, odd -> kout
+    for (int p = 0; p < PASSES; ++p) {
+        const bool to_alt = (p % 2 == 0);
+        const T* ksrc = p == 0 ? kin : (to_alt ? kout : kalt);
+        T* kdst = to_alt ? kalt : kout;
+        const V* vsrc = nullptr;
+        V* vdst = nullptr;
+        if constexpr (MODE != SORT_KEYS) {
+            vsrc = p == 0 ? vin : (to_alt ? vout : valt);
+            vdst = to_alt ? valt : vout;
+        }
+        const bool wk = keys_out || (p + 1 < PASSES);
+        launch_pass<T, V, MODE>(c, ksrc, kdst, vsrc, vdst, n, 8 * p, desc, p, g_offs + p * RADIX,
+                                counters + p, wk);
+    }
+}
+
+}  // namespace
+
+template <typename T, typename V>
+void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vin, V* vout,
+                V* valt, std::uint64_t n, bool desc, bool keys_out) {
+    switch (mode) {
+        case SORT_KEYS:
+            radix_sort_impl<T, V, SORT_KEYS>(c, kin, kout, kalt, nullptr, nullptr, nullptr, n, desc,
+                                             true);
+            break;
+        case SORT_PAIRS:
+            radix_sort_impl<T, V, SORT_PAIRS>(c, kin, kout, kalt, vin, vout, valt, n, desc, true);
+            break;
+        case SORT_IOTA:
+            radix_sort_impl<T, V, SORT_IOTA>(c, kin, kout, kalt, nullptr, vout, valt, n, desc,
+                                             keys_out);
+            break;
+        case SORT_LOWMEM:
+            radix_sort_impl<T, V, SORT_LOWMEM>(c, kin, nullptr, nullptr, nullptr, vout, valt, n,
+                                               desc, false);
+            break;
+        default:
+            throw invalid_argument("radix_sort: unknown mode");
+    }
+}
+
+std::uint64_t radix_tile_items(int key_bytes, int) {
+    return key_bytes == 8 ? tile_cfg<std::uint64_t>::TILE : tile_cfg<std::uint32_t>::TILE;
+}
+
+#define AKB_INST(T, V)                                                                          \
+    template void radix_sort<T, V>(ak_ctx*, int, const T*, T*, T*, const V*, V*, V*,           \
+                                   std::uint64_t, bool, bool);
+#define AKB_INST_K(T)                  \
+    AKB_INST(T, std::uint32_t)         \
+    AKB_INST(T, std::int32_t)          \
+    AKB_INST(T, std::uint64_t)         \
+    AKB_INST(T, std::int64_t)
+
+AKB_INST_K(std::int32_t)
+AKB_INST_K(std::uint32_t)
+AKB_INST_K(std::int64_t)
+AKB_INST_K(std::uint64_t)
+AKB_INST_K(float)
+AKB_INST_K(double)
+
+}  // namespace akb

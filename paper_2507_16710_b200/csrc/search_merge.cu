@@ -1,0 +1,214 @@
+// search_merge.cu -- searchsorted, sample gather, merge-path 2-way merge, is_sorted.
+#include "search_merge.cuh"
+
+namespace akb {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ std::uint64_t lower_bound_dev(const T* h, std::uint64_t n, T v, bool desc) {
+    std::uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const std::uint64_t mid = lo + (hi - lo) / 2;
+        if (key_less(h[mid], v, desc)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+template <typename T>
+__device__ __forceinline__ std::uint64_t upper_bound_dev(const T* h, std::uint64_t n, T v, bool desc) {
+    std::uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const std::uint64_t mid = lo + (hi - lo) / 2;
+        if (!key_less(v, h[mid], desc)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <typename T>
+__global__ void search_kernel(const T* __restrict__ hay, std::uint64_t n, const T* __restrict__ needles,
+                              std::uint64_t m, int side_last, int desc, std::uint64_t* __restrict__ out) {
+    const std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const T v = needles[i];
+    out[i] = side_last ? upper_bound_dev(hay, n, v, desc != 0) : lower_bound_dev(hay, n, v, desc != 0);
+}
+
+template <typename T>
+__global__ void gather_kernel(const T* __restrict__ x, std::uint64_t n, std::uint64_t k, T* __restrict__ out) {
+    const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j == 0) {
+        out[0] = x[0];
+        out[1] = x[n - 1];
+    }
+    if (j >= k) return;
+    std::uint64_t pos;
+    if (k == 1) pos = n / 2;
+    else pos = (2 * j * (n - 1) + (k - 1)) / (2 * (k - 1));  // sihsort.hpp:279
+    out[2 + j] = x[pos];
+}
+
+// co_rank of sort.hpp:75-88: #elements of a among the first k merged outputs.
+template <typename T>
+__device__ __forceinline__ std::uint64_t co_rank_dev(std::uint64_t k, const T* a, std::uint64_t na,
+                                                     const T* b, std::uint64_t nb, bool desc) {
+    std::uint64_t lo = k > nb ? k - nb : 0;
+    std::uint64_t hi = k < na ? k : na;
+    while (lo < hi) {
+        const std::uint64_t i = lo + (hi - lo) / 2;
+        if (key_less(b[k - i - 1], a[i], desc)) hi = i;
+        else lo = i + 1;
+    }
+    return lo;
+}
+
+constexpr int MERGE_BLOCK = 256;
+template <typename T>
+struct merge_cfg {
+    static constexpr int ITEMS = sizeof(T) == 8 ? 12 : 16;
+    static constexpr int TILE = MERGE_BLOCK * ITEMS;
+};
+
+template <typename T>
+__global__ void merge_partition_kernel(const T* __restrict__ a, std::uint64_t na, const T* __restrict__ b,
+                                       std::uint64_t nb, std::uint64_t tiles, int desc,
+                                       std::uint64_t* __restrict__ split) {
+    const std::uint64_t t = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t > tiles) return;
+    std::uint64_t diag = t * merge_cfg<T>::TILE;
+    if (diag > na + nb) diag = na + nb;
+    split[t] = co_rank_dev(diag, a, na, b, nb, desc != 0);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(MERGE_BLOCK)
+    merge_kernel(const T* __restrict__ a, std::uint64_t na, const T* __restrict__ b, std::uint64_t nb,
+                 const std::uint64_t* __restrict__ split, T* __restrict__ dst, int desc) {
+    constexpr int ITEMS = merge_cfg<T>::ITEMS;
+    constexpr int TILE = merge_cfg<T>::TILE;
+    __shared__ T s[TILE];
+    const bool dsc = desc != 0;
+    const std::uint64_t t = blockIdx.x;
+    const std::uint64_t d0 = t * TILE;
+    std::uint64_t d1 = d0 + TILE;
+    if (d1 > na + nb) d1 = na + nb;
+    const std::uint64_t a0 = split[t], a1 = split[t + 1];
+    const std::uint64_t b0 = d0 - a0, b1 = d1 - a1;
+    const int la = static_cast<int>(a1 - a0), lb = static_cast<int>(b1 - b0);
+    for (int i = threadIdx.x; i < la; i += MERGE_BLOCK) s[i] = a[a0 + i];
+    for (int i = threadIdx.x; i < lb; i += MERGE_BLOCK) s[la + i] = b[b0 + i];
+    __syncthreads();
+    const T* sa = s;
+    const T* sb = s + la;
+    const int total = la + lb;
+    T outv[ITEMS];
+    const int k0 = threadIdx.x * ITEMS;
+    int cnt = 0;
+    if (k0 < total) {
+        int ai = static_cast<int>(co_rank_dev<T>(k0, sa, la, sb, lb, dsc));
+        int bi = k0 - ai;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (k0 + j < total) {
+                const bool take_a = ai < la && (bi >= lb || !key_less(sb[bi], sa[ai], dsc));
+                outv[j] = take_a ? sa[ai] : sb[bi];
+                ai += take_a ? 1 : 0;
+                bi += take_a ? 0 : 1;
+                ++cnt;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j)
+        if (j < cnt) s[k0 + j] = outv[j];
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += MERGE_BLOCK) dst[d0 + i] = s[i];
+}
+
+template <typename T>
+__global__ void unsorted_kernel(const T* __restrict__ x, std::uint64_t n, int desc, unsigned* flag) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    bool bad = false;
+    for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i + 1 < n;
+         i += stride)
+        bad |= key_less(x[i + 1], x[i], desc != 0);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+}  // namespace
+
+template <typename T>
+void searchsorted(ak_ctx* c, const T* hay, std::uint64_t n, const T* needles, std::uint64_t m,
+                  int side_last, int desc, std::uint64_t* d_out) {
+    if (m == 0) return;
+    const unsigned blocks = static_cast<unsigned>(ceil_div(m, 256));
+    search_kernel<T><<<blocks, 256, 0, c->stream>>>(hay, n, needles, m, side_last, desc, d_out);
+    AKB_CUDA(cudaGetLastError());
+    c->kernel_launches += 1;
+}
+
+template <typename T>
+std::uint64_t gather_samples(ak_ctx* c, const T* sorted, std::uint64_t n, std::uint64_t k, T* d_out) {
+    if (n == 0) return 0;
+    if (k > n) k = n;
+    const unsigned blocks = static_cast<unsigned>(ceil_div(k > 0 ? k : 1, 256));
+    gather_kernel<T><<<blocks, 256, 0, c->stream>>>(sorted, n, k, d_out);
+    AKB_CUDA(cudaGetLastError());
+    c->kernel_launches += 1;
+    return k;
+}
+
+template <typename T>
+void merge2(ak_ctx* c, const T* a, std::uint64_t na, const T* b, std::uint64_t nb, T* dst, bool desc) {
+    const std::uint64_t total = na + nb;
+    if (total == 0) return;
+    if (nb == 0 || na == 0) {
+        const T* src = na ? a : b;
+        if (src != dst)
+            AKB_CUDA(cudaMemcpyAsync(dst, src, total * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    const std::uint64_t tiles = ceil_div(total, merge_cfg<T>::TILE);
+    std::uint64_t* split = ctx_split(c, tiles + 1);
+    merge_partition_kernel<T><<<static_cast<unsigned>(ceil_div(tiles + 1, 256)), 256, 0, c->stream>>>(
+        a, na, b, nb, tiles, desc ? 1 : 0, split);
+    AKB_CUDA(cudaGetLastError());
+    const int tok = ctx_prof_begin(c, KF_MERGE);
+    merge_kernel<T><<<static_cast<unsigned>(tiles), MERGE_BLOCK, 0, c->stream>>>(a, na, b, nb, split, dst,
+                                                                                desc ? 1 : 0);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 2;
+}
+
+template <typename T>
+bool is_sorted(ak_ctx* c, const T* x, std::uint64_t n, bool desc) {
+    if (n < 2) return true;
+    unsigned* flag = reinterpret_cast<unsigned*>(static_cast<char*>(c->small) + 196608);
+    AKB_CUDA(cudaMemsetAsync(flag, 0, 4, c->stream));
+    unsorted_kernel<T><<<c->sm_count * 4, 256, 0, c->stream>>>(x, n, desc ? 1 : 0, flag);
+    AKB_CUDA(cudaGetLastError());
+    c->kernel_launches += 1;
+    unsigned* h = static_cast<unsigned*>(ctx_pinned(c, 4));
+    AKB_CUDA(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));
+    return *h == 0;
+}
+
+#define AKB_INST(T)                                                                               \
+    template void searchsorted<T>(ak_ctx*, const T*, std::uint64_t, const T*, std::uint64_t, int,  \
+                                  int, std::uint64_t*);                                           \
+    template std::uint64_t gather_samples<T>(ak_ctx*, const T*, std::uint64_t, std::uint64_t, T*);  \
+    template void merge2<T>(ak_ctx*, const T*, std::uint64_t, const T*, std::uint64_t, T*, bool);   \
+    template bool is_sorted<T>(ak_ctx*, const T*, std::uint64_t, bool);
+
+AKB_INST(std::int32_t)
+AKB_INST(std::uint32_t)
+AKB_INST(std::int64_t)
+AKB_INST(std::uint64_t)
+AKB_INST(float)
+AKB_INST(double)
+
+}  // namespace akb

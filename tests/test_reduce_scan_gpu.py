@@ -1,0 +1,154 @@
+"""GPU parity: reduce / mapreduce / accumulate / searchsorted vs the oracle.
+
+Integers: bit-exact. Float32: reduce rel <= 1e-5 and scan per-element rel <= 1e-5
+against the f64 oracle (the reference's own f32 fold is not authoritative at
+2^30; tolerance from reference tests/test_primitives.cpp:103-111).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-5
+
+
+def approx_rel(got, want, rel):  # tests/test_utils.hpp:109-112
+    scale = max(1.0, abs(got), abs(want))
+    return abs(got - want) <= rel * scale
+
+
+def vals(rng, dt, n):  # tests/test_utils.hpp:30-38
+    dt = np.dtype(dt)
+    if dt.kind == "f":
+        return rng.uniform(0, 1, n).astype(dt)
+    if dt.kind == "u":
+        return rng.integers(0, 10001, n).astype(dt)
+    return rng.integers(-10000, 10001, n).astype(dt)
+
+
+def t(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def test_reduce_known_answers(ak, ex, dev):
+    d = t(np.arange(1, 101, dtype=np.int64), dev)  # test_primitives.cpp:36-46
+    assert ak.reduce("sum", d, 0, ex) == 5050
+    sentinel = np.iinfo(np.int64).min
+    assert ak.reduce("max", torch.empty(0, dtype=torch.int64, device=dev), int(sentinel), ex) == sentinel
+    assert ak.mapreduce("abs", "max", t(np.array([-3, 1, 2], dtype=np.int32), dev), 0, ex) == 3
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.uint64, np.float32, np.float64])
+@pytest.mark.parametrize("n", [1, 3, 100_000, 1_000_003])
+@pytest.mark.parametrize("op", ["sum", "min", "max"])
+@pytest.mark.parametrize("mapf", ["identity", "abs", "square"])
+def test_reduce_matches_oracle(ak, orc, ex, dev, dt, n, op, mapf):
+    if mapf == "abs" and np.dtype(dt).kind == "u":
+        pytest.skip("abs on unsigned is identity")
+    rng = np.random.default_rng(n + len(op))
+    x = vals(rng, dt, n)
+    got = ak.mapreduce(mapf, op, t(x, dev), None, ex)
+    want = orc.reduce(x, op, mapf)
+    if np.dtype(dt).kind == "f" and op == "sum":
+        assert approx_rel(float(got), float(want), F32_TOL if dt == np.float32 else 1e-12)
+    elif np.dtype(dt) == np.float32 and mapf == "square":
+        assert approx_rel(float(got), float(want), F32_TOL)
+    else:
+        assert got == want
+
+
+def test_reduce_misaligned_views(ak, orc, ex, dev):
+    x = vals(np.random.default_rng(1), np.int64, 100_000)
+    d = t(x, dev)
+    for off in range(1, 4):
+        assert ak.reduce("sum", d[off:], 0, ex) == orc.reduce(x[off:])
+
+
+def test_accumulate_known_answers(ak, ex, dev):
+    inc = ak.accumulate("sum", t(np.ones(4, dtype=np.int32), dev), ex=ex)  # test_primitives.cpp:113-121
+    assert inc.cpu().tolist() == [1, 2, 3, 4]
+    exc = ak.accumulate("sum", t(np.array([1, 2, 3], dtype=np.int32), dev), inclusive=False, ex=ex)
+    assert exc.cpu().tolist() == [0, 1, 3]
+    d = t(np.array([5, 4, 3, 2, 1], dtype=np.int32), dev)  # in place, test_primitives.cpp:138-151
+    ak.accumulate("sum", d, out=d, chunk_size=2, ex=ex)
+    assert d.cpu().tolist() == [5, 9, 12, 14, 15]
+    with pytest.raises(ak.InvalidArgument):
+        ak.accumulate("sum", d, out=torch.zeros(4, dtype=torch.int32, device=dev), ex=ex)
+    with pytest.raises(ak.InvalidArgument):
+        ak.accumulate("sum", d, chunk_size=0, ex=ex)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.uint64])
+@pytest.mark.parametrize("n", [1, 1000, 4096, 4097, 100_000, 3_000_017])
+@pytest.mark.parametrize("inclusive", [True, False])
+def test_accumulate_int_exact(ak, orc, ex, dev, dt, n, inclusive):
+    x = vals(np.random.default_rng(n), dt, n)
+    init = 100 if dt != np.uint64 else 0  # non-neutral init seeds position 0 (scan.hpp:12-16)
+    got = ak.accumulate("sum", t(x, dev), inclusive=inclusive, init=init, ex=ex).cpu().numpy()
+    if dt == np.uint64:
+        want = np.cumsum(x, dtype=np.uint64)
+        if not inclusive:
+            want = np.concatenate([[0], want[:-1]]).astype(np.uint64)
+    else:
+        want = orc.scan(x, inclusive, init)
+    assert np.array_equal(got, want)
+
+
+def test_accumulate_minmax(ak, ex, dev):
+    x = vals(np.random.default_rng(9), np.int64, 50_000)
+    got = ak.accumulate("max", t(x, dev), init=np.iinfo(np.int64).min, ex=ex).cpu().numpy()
+    assert np.array_equal(got, np.maximum.accumulate(x))
+    got = ak.accumulate("min", t(x, dev), init=np.iinfo(np.int64).max, ex=ex).cpu().numpy()
+    assert np.array_equal(got, np.minimum.accumulate(x))
+
+
+@pytest.mark.parametrize("n", [10, 100_000, 5_000_000])
+def test_accumulate_f32_tolerance(ak, orc, ex, dev, n):
+    x = vals(np.random.default_rng(n), np.float32, n)
+    got = ak.accumulate("sum", t(x, dev), ex=ex).cpu().numpy().astype(np.float64)
+    want = orc.scan(x)
+    rel = np.abs(got - want) / np.maximum(1.0, np.abs(want))
+    assert rel.max() <= F32_TOL
+
+
+def test_config3_full_size(ak, ex, dev):
+    """BASELINE config 3 at 2^30: reduce == last scan element (i64, exact); f32 vs fp64 torch."""
+    n = 1 << 30
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    x = torch.randint(-10000, 10001, (n,), dtype=torch.int64, device=dev, generator=g)
+    s = ak.reduce("sum", x, 0, ex)
+    sc = ak.accumulate("sum", x, ex=ex)
+    assert int(sc[-1]) == s == int(x.sum())
+    assert torch.equal(sc[1:] - sc[:-1], x[1:])  # exact differences
+    del sc
+    xf = torch.rand(n, dtype=torch.float32, device=dev, generator=g)
+    want = float(xf.double().sum())
+    got = ak.reduce("sum", xf, 0.0, ex)
+    assert approx_rel(got, want, F32_TOL)
+    scf = ak.accumulate("sum", xf, ex=ex)
+    ref = torch.cumsum(xf.double(), 0)
+    rel = ((scf.double() - ref).abs() / ref.abs().clamp_min(1.0)).max().item()
+    assert rel <= F32_TOL
+
+
+def test_searchsorted_known_answers(ak, ex, dev):
+    hay = t(np.array([1, 2, 4, 4, 7], dtype=np.int32), dev)  # test_primitives.cpp:164-175
+    nd = t(np.array([4, 0, 9], dtype=np.int32), dev)
+    assert ak.searchsorted(hay, nd, "first", ex).cpu().tolist() == [2, 0, 5]
+    assert ak.searchsorted(hay, nd, "last", ex).cpu().tolist() == [4, 0, 5]
+    uns = t(np.array([3, 1, 2], dtype=np.int32), dev)  # :197-204
+    ak.searchsorted(uns, t(np.array([2], dtype=np.int32), dev), "first", ex)
+    with pytest.raises(ak.InvalidArgument):
+        ak.searchsorted(uns, t(np.array([2], dtype=np.int32), dev), "first", ex, validate=True)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.uint64, np.float32, np.float64])
+def test_searchsorted_matches_oracle(ak, orc, ex, dev, dt):
+    rng = np.random.default_rng(13)  # test_primitives.cpp:177-195 (2000 hay, 500 needles)
+    hay = np.sort(vals(rng, dt, 2000))
+    nd = vals(rng, dt, 500)
+    for side in ("first", "last"):
+        got = ak.searchsorted(t(hay, dev), t(nd, dev), side, ex).cpu().numpy().astype(np.uint64)
+        assert np.array_equal(got, orc.searchsorted(hay, nd, side))

@@ -1,0 +1,150 @@
+"""GPU parity: SIHSort on one GPU with P logical ranks (loopback world) vs the oracle.
+
+Per-rank outputs AND per-rank sih_stats must equal the oracle's exactly (the
+oracle itself equals the reference's sihsort over sim::world, tests/test_oracle.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def dist(rng, kind, n, dt, r):
+    dt = np.dtype(dt)
+    if kind == "uniform":
+        info = np.iinfo(dt) if dt.kind in "iu" else None
+        if info is not None:
+            return rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        return rng.uniform(-1e6, 1e6, n).astype(dt)
+    if kind == "zipf":
+        return np.minimum(rng.zipf(1.1, n), 10**6).astype(dt)
+    if kind == "equal":
+        return np.full(n, 42, dtype=dt)
+    if kind == "sorted":
+        return (np.arange(n) + r * n).astype(dt)
+    if kind == "reversed":
+        return (np.arange(n)[::-1] + (7 - r) * n).astype(dt)
+    raise ValueError(kind)
+
+
+def run(ak, orc, dev, ins, cfg=None):
+    outs, stats = ak.sihsort_loopback([torch.from_numpy(a).to(dev) for a in ins], cfg)
+    want, wstats, _ = orc.sihsort(ins, orc.SihConfig(*(cfg.sample_per_rank, cfg.bins, cfg.max_refine_rounds,
+                                                     cfg.imbalance_tol)) if cfg else None)
+    for r in range(len(ins)):
+        assert np.array_equal(outs[r].cpu().numpy(), want[r]), f"rank {r} output"
+        assert stats[r].as_dict() == wstats[r], f"rank {r} stats"
+    return outs, stats
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("kind", ["uniform", "zipf", "equal", "sorted", "reversed"])
+def test_sihsort_matches_oracle(ak, orc, dev, P, kind):
+    rng = np.random.default_rng(P * 100 + len(kind))
+    ins = [dist(rng, kind, 10_000, np.int64, r) for r in range(P)]
+    run(ak, orc, dev, ins)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64, np.float32, np.float64])
+def test_sihsort_dtypes(ak, orc, dev, dt):
+    rng = np.random.default_rng(77)
+    ins = [dist(rng, "uniform", 5_000 + 13 * r, dt, r) for r in range(4)]
+    run(ak, orc, dev, ins)
+
+
+def test_sihsort_bench_keys_p8(ak, orc, dev):
+    ins = [ak.bench_keys(42, r, 100_000, np.int64) for r in range(8)]
+    outs, stats = run(ak, orc, dev, ins)
+    mean = sum(len(o) for o in outs) / 8
+    assert max(len(o) for o in outs) <= 1.25 * mean  # SPEC acceptance 6
+
+
+def test_sihsort_known_answers(ak, orc, dev):
+    outs, _ = run(ak, orc, dev, [np.array([r], dtype=np.int64) for r in range(4)])
+    assert [o.cpu().tolist() for o in outs] == [[0], [1], [2], [3]]
+    outs, stats = run(ak, orc, dev, [np.full(1000, 5, dtype=np.int64) for _ in range(4)])
+    assert [len(o) for o in outs] == [4000, 0, 0, 0]
+    assert stats[0].rounds_used == 4 and stats[0].converged == 0
+
+
+def test_sihsort_empty_and_ragged(ak, orc, dev):
+    rng = np.random.default_rng(5)
+    ins = [np.empty(0, dtype=np.int64), dist(rng, "uniform", 3, np.int64, 1),
+           np.empty(0, dtype=np.int64), dist(rng, "uniform", 9000, np.int64, 3)]
+    run(ak, orc, dev, ins)
+    run(ak, orc, dev, [np.empty(0, dtype=np.int64)] * 3)
+
+
+def test_sihsort_config_variants(ak, orc, dev):
+    rng = np.random.default_rng(6)
+    ins = [dist(rng, "zipf", 8000, np.int64, r) for r in range(4)]
+    for cfg in (ak.SihConfig(7, 3, 0, 0.25), ak.SihConfig(0, 0, 1, 0.01), ak.SihConfig(1, 1, 4, 0.5)):
+        run(ak, orc, dev, ins, cfg)
+
+
+def test_sihsort_capacity_error(ak, dev):
+    ins = [torch.full((1000,), 5, dtype=torch.int64, device=dev) for _ in range(2)]
+    with pytest.raises(ak.CapacityError):
+        ak.sihsort_loopback(ins, capacity=1500)
+
+
+def test_sihsort_single_rank_api(ak, orc, ex, dev):
+    x = ak.bench_keys(42, 0, 200_000, np.int64)
+    out, st = ak.sihsort(torch.from_numpy(x).to(dev), None, None, ex)
+    want, wst, _ = orc.sihsort([x])
+    assert np.array_equal(out.cpu().numpy(), want[0])
+    assert st.as_dict() == wst[0]
+    h, st2 = ak.sihsort_host(x, None, None, ex)
+    assert np.array_equal(h, want[0])
+
+
+def fingerprint(t):
+    """Order-independent multiset fingerprint: (count, sum, xor) of a 64-bit mix."""
+    x = t.view(torch.int64)
+    z = x * -7046029254386353131  # wraps (0x9e3779b97f4a7c15 as int64)
+    z = z ^ ((z >> 31) & ((1 << 33) - 1))
+    return int(t.numel()), int(z.sum()), int(_xor_all(z))
+
+
+def _xor_all(z):
+    while z.numel() > 1:
+        if z.numel() % 2:
+            z = torch.cat([z, torch.zeros(1, dtype=z.dtype, device=z.device)])
+        z = z[0::2] ^ z[1::2]
+    return z[0]
+
+
+@pytest.mark.parametrize("dt,n", [(np.int64, 1 << 28), (np.uint64, 1 << 30)])
+def test_config45_full_size_single_rank(ak, ex, dev, dt, n):
+    """BASELINE configs 4/5 at full per-GPU size (P=1 here): sortedness + multiset fingerprint."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(45)
+    x = torch.randint(-(1 << 62), 1 << 62, (n,), dtype=torch.int64, device=dev, generator=g)
+    if dt == np.uint64:
+        x = x.view(torch.uint64)
+    out, st = ak.sihsort(x, None, None, ex, capacity=n)
+    assert out.numel() == n and st.output_count == n
+    o = out.view(torch.int64)
+    if dt == np.uint64:
+        o = o ^ (-(1 << 63))  # order-preserving map uint64 -> int64
+    assert bool((o[1:] >= o[:-1]).all())
+    assert fingerprint(out) == fingerprint(x)
+
+
+def test_sihsort_p8_large_properties(ak, dev):
+    """8 logical ranks x 2^22 bench keys: global order, boundaries, multiset, balance."""
+    P, n = 8, 1 << 22
+    ins = [torch.from_numpy(ak.bench_keys(42, r, n, np.int64)).to(dev) for r in range(P)]
+    outs, stats = ak.sihsort_loopback(ins)
+    for r in range(P):
+        o = outs[r]
+        if o.numel() > 1:
+            assert bool((o[1:] >= o[:-1]).all())
+        if r + 1 < P and o.numel() and outs[r + 1].numel():
+            assert int(o[-1]) <= int(outs[r + 1][0])
+    allin = torch.cat(ins)
+    allout = torch.cat(outs)
+    assert fingerprint(allin) == fingerprint(allout)
+    assert max(o.numel() for o in outs) <= 1.25 * n
+    assert all(s.converged == 1 for s in stats)
