@@ -159,7 +159,17 @@ class ExecBackend:
 
     @property
     def handle(self) -> C.c_void_p:
+        """The C handle; ordering point: work queued on torch's current stream (e.g. the
+        producer of an input tensor) completes before the ctx stream runs the next op."""
+        cur = torch.cuda.current_stream(self.device)
+        if cur.cuda_stream != self.stream.cuda_stream:
+            self.stream.wait_stream(cur)
         return self._h
+
+    def fence(self) -> None:
+        """Make torch's current stream wait for everything queued on the ctx stream
+        (only needed after non-blocking calls)."""
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def set_blocking(self, blocking: bool) -> None:
         _check(_fn("ak_ctx_set_blocking", [_P, C.c_int])(self._h, int(blocking)))

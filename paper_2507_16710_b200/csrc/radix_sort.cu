@@ -1,4 +1,20 @@
 // radix_sort.cu -- onesweep radix sort kernels (see radix_sort.cuh).
+//
+// Pass kernel structure (one CTA per tile, tiles claimed in launch order):
+//   1. load the tile (warp-striped, coalesced) and extract 8-bit digits once
+//      (packed 4 per register);
+//   2. EARLY COUNTS: block digit histogram with shared atomics, published to the
+//      look-back chain immediately (AGG, or INC for tile 0), so successors see
+//      this tile's counts before it has ranked anything;
+//   3. stable warp ranking: hardware match.any (or 8 ballots) per item, leader
+//      bumps the warp's digit counter;
+//   4. warp-exclusive offsets + block scan of digit totals -> digit-ordered
+//      staging of keys (and payload) in shared memory;
+//   5. windowed decoupled look-back (4 predecessors in flight per digit) ->
+//      INC publish and global digit bases;
+//   6. scatter contiguous per-digit runs.
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "radix_sort.cuh"
@@ -10,29 +26,42 @@ namespace {
 constexpr int RADIX = 256;
 constexpr std::uint32_t FULL = 0xffffffffu;
 
-template <typename T>
+template <typename T, typename V, int MODE>
 struct tile_cfg {
     static constexpr int BLOCK = 384;
-    static constexpr int ITEMS = sizeof(T) == 8 ? 16 : 16;
+    static constexpr bool HAS_VALS = MODE != SORT_KEYS;
+    static constexpr int ITEMS = !HAS_VALS ? 16 : (sizeof(T) + sizeof(V) <= 8 ? 16 : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
     static constexpr int TILE = BLOCK * ITEMS;
     static constexpr int MIN_BLOCKS = 2;
 };
 
 template <typename T>
 __device__ __forceinline__ std::uint32_t digit_of(T key, int shift, bool desc) {
-    return static_cast<std::uint32_t>((ordered(key, desc) >> shift) & 0xffu);
+    const auto o = ordered(key, desc);
+    if constexpr (sizeof(o) == 8) {
+        const std::uint32_t w = shift >= 32 ? static_cast<std::uint32_t>(o >> 32) : static_cast<std::uint32_t>(o);
+        return (w >> (shift & 31)) & 0xffu;
+    } else {
+        return (o >> shift) & 0xffu;
+    }
 }
 
-// Lanes holding the same 8-bit digit, via 8 ballots.
+// Lanes holding the same 8-bit digit.
+template <bool HW>
 __device__ __forceinline__ std::uint32_t match_digit(std::uint32_t d) {
-    std::uint32_t m = FULL;
+    if constexpr (HW) {
+        return __match_any_sync(FULL, d);
+    } else {
+        std::uint32_t m = FULL;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-        const bool bit = (d >> b) & 1u;
-        const std::uint32_t bal = __ballot_sync(FULL, bit);
-        m &= bit ? bal : ~bal;
+        for (int b = 0; b < 8; ++b) {
+            const std::uint32_t bal = __ballot_sync(FULL, (d >> b) & 1u);
+            // all-ones when bit b of d is clear -> keep lanes whose bit is clear too
+            const std::uint32_t flip = 0u - (((d >> b) & 1u) ^ 1u);
+            m &= bal ^ flip;
+        }
+        return m;
     }
-    return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -89,8 +118,7 @@ __global__ void __launch_bounds__(256) hist_kernel(const T* __restrict__ keys, s
         std::uint32_t s = 0;
 #pragma unroll
         for (int q = 0; q < PARTS; ++q) s += sh[i * PARTS + q];
-        if (s) atomicAdd(reinterpret_cast<unsigned long long*>(g_hist + i),
-                         static_cast<unsigned long long>(s));
+        if (s) atomicAdd(reinterpret_cast<unsigned long long*>(g_hist + i), static_cast<unsigned long long>(s));
     }
 }
 
@@ -118,39 +146,44 @@ __global__ void __launch_bounds__(RADIX) hist_scan_kernel(const std::uint64_t* _
 // ---------------------------------------------------------------------------
 template <typename T, typename V, int MODE>
 struct pass_smem {
-    static constexpr int BLOCK = tile_cfg<T>::BLOCK;
-    static constexpr int TILE = tile_cfg<T>::TILE;
+    using C = tile_cfg<T, V, MODE>;
+    static constexpr int BLOCK = C::BLOCK;
+    static constexpr int TILE = C::TILE;
     static constexpr int WARPS = BLOCK / 32;
     static constexpr bool HAS_KEYS_SMEM = MODE != SORT_LOWMEM;
-    static constexpr bool HAS_VALS = MODE != SORT_KEYS;
+    static constexpr bool HAS_VALS = C::HAS_VALS;
     static constexpr std::size_t keys_off = 0;
     static constexpr std::size_t keys_bytes = HAS_KEYS_SMEM ? sizeof(T) * TILE : 0;
     static constexpr std::size_t vals_off = keys_off + keys_bytes;
     static constexpr std::size_t vals_bytes = HAS_VALS ? sizeof(V) * TILE : 0;
     static constexpr std::size_t whist_off = (vals_off + vals_bytes + 15) & ~std::size_t(15);
     static constexpr std::size_t whist_bytes = sizeof(std::uint32_t) * WARPS * RADIX;
-    static constexpr std::size_t gofs_off = whist_off + whist_bytes;
+    static constexpr std::size_t hist_off = whist_off + whist_bytes;
+    static constexpr std::size_t hist_bytes = sizeof(std::uint32_t) * RADIX;
+    static constexpr std::size_t gofs_off = hist_off + hist_bytes;
     static constexpr std::size_t gofs_bytes = sizeof(std::uint64_t) * RADIX;
     static constexpr std::size_t misc_off = gofs_off + gofs_bytes;
     static constexpr std::size_t misc_bytes = sizeof(std::uint32_t) * 16;
     static constexpr std::size_t total = misc_off + misc_bytes;
 };
 
-template <typename T, typename V, int MODE>
-__global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
+template <typename T, typename V, int MODE, bool HW_MATCH>
+__global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MODE>::MIN_BLOCKS)
     onesweep_kernel(const T* __restrict__ kin, T* __restrict__ kout, const V* __restrict__ vin,
                     V* __restrict__ vout, std::uint64_t n, int shift, int desc, int pass_index,
                     const std::uint64_t* __restrict__ goffs, std::uint64_t* lookback,
                     std::uint32_t* tile_counter, std::uint32_t tag, int write_keys) {
     using L = pass_smem<T, V, MODE>;
     constexpr int BLOCK = L::BLOCK;
-    constexpr int ITEMS = tile_cfg<T>::ITEMS;
+    constexpr int ITEMS = tile_cfg<T, V, MODE>::ITEMS;
     constexpr int TILE = L::TILE;
     constexpr int WARPS = L::WARPS;
+    constexpr int DW = (ITEMS + 3) / 4;  // packed digit words
     extern __shared__ __align__(16) unsigned char smem[];
     T* s_keys = reinterpret_cast<T*>(smem + L::keys_off);
     V* s_vals = reinterpret_cast<V*>(smem + L::vals_off);
     std::uint32_t* s_whist = reinterpret_cast<std::uint32_t*>(smem + L::whist_off);
+    std::uint32_t* s_hist = reinterpret_cast<std::uint32_t*>(smem + L::hist_off);
     std::uint64_t* s_gofs = reinterpret_cast<std::uint64_t*>(smem + L::gofs_off);
     std::uint32_t* s_misc = reinterpret_cast<std::uint32_t*>(smem + L::misc_off);
 
@@ -158,20 +191,26 @@ __global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
     const bool dsc = desc != 0;
     if (tid == 0) s_misc[0] = atomicAdd(tile_counter, 1u);
     for (int i = tid; i < WARPS * RADIX; i += BLOCK) s_whist[i] = 0;
+    if (tid < RADIX) s_hist[tid] = 0;
     __syncthreads();
     const std::uint32_t tile = s_misc[0];
     const std::uint64_t tile_base = static_cast<std::uint64_t>(tile) * TILE;
     const std::uint64_t remaining = n - tile_base;
     const std::uint32_t valid = remaining < TILE ? static_cast<std::uint32_t>(remaining) : TILE;
-    const std::uint64_t wbase = tile_base + static_cast<std::uint64_t>(warp) * 32 * ITEMS;
+    const bool full = valid == TILE;
+    const std::uint32_t wofs = static_cast<std::uint32_t>(warp) * 32 * ITEMS + lane;  // tile-local index of item 0
 
-    // ---- load (warp-striped: item i of lane l is key wbase + 32 i + l) ----
+    // ---- load (warp-striped: item i of lane l is tile-local wofs + 32 i) ----
     T k[ITEMS];
     V v[ITEMS];
+    std::uint32_t dg[DW];
+#pragma unroll
+    for (int w = 0; w < DW; ++w) dg[w] = 0;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const std::uint64_t idx = wbase + i * 32 + lane;
-        const bool ok = idx < n;
+        const std::uint32_t li = wofs + i * 32;
+        const bool ok = full || li < valid;
+        const std::uint64_t idx = tile_base + li;
         if constexpr (MODE == SORT_LOWMEM) {
             if (ok) {
                 const V ix = pass_index == 0 ? static_cast<V>(idx) : vin[idx];
@@ -184,36 +223,49 @@ __global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
         } else {
             k[i] = ok ? kin[idx] : T(0);
             if constexpr (MODE == SORT_PAIRS) v[i] = ok ? vin[idx] : V(0);
-            if constexpr (MODE == SORT_IOTA) v[i] = static_cast<V>(idx);
+            if constexpr (MODE == SORT_IOTA)
+                v[i] = pass_index == 0 ? static_cast<V>(idx) : (ok ? vin[idx] : V(0));
         }
+    }
+    // ---- digits + early counts ----
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint32_t li = wofs + i * 32;
+        const bool ok = full || li < valid;
+        const std::uint32_t d = ok ? digit_of(k[i], shift, dsc) : 255u;  // padding sorts last
+        dg[i / 4] |= d << (8 * (i % 4));
+        if (ok) atomicAdd(s_hist + d, 1u);
+    }
+    __syncthreads();
+    std::uint64_t* my_lb = lookback + static_cast<std::uint64_t>(tile) * RADIX + tid;
+    const std::uint64_t tagbits = static_cast<std::uint64_t>(tag) << LB_TAG_SHIFT;
+    std::uint32_t count = 0;
+    if (tid < RADIX) {
+        count = s_hist[tid];
+        st_relaxed_u64(my_lb, (tile == 0 ? LB_INC : LB_AGG) | tagbits | count);
     }
 
     // ---- warp-level stable ranking ----
-    std::uint32_t rk[ITEMS];
+    std::uint32_t rk[(ITEMS + 1) / 2];  // warp-local ranks (< 32*ITEMS), two 16-bit per word
+#pragma unroll
+    for (int w = 0; w < (ITEMS + 1) / 2; ++w) rk[w] = 0;
     std::uint32_t* wh = s_whist + warp * RADIX;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const std::uint64_t idx = wbase + i * 32 + lane;
-        const std::uint32_t d = idx < n ? digit_of(k[i], shift, dsc) : 255u;
-        const std::uint32_t peers = match_digit(d);
-        const int leader = __ffs(peers) - 1;
+        const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+        const std::uint32_t peers = match_digit<HW_MATCH>(d);
+        const int leader = 31 - __clz(peers);
         const std::uint32_t below = __popc(peers & lanemask_lt());
         std::uint32_t base = 0;
-        if (lane == leader) {
-            base = wh[d];
-            wh[d] = base + __popc(peers);
-        }
+        if (lane == leader) base = atomicAdd(wh + d, static_cast<std::uint32_t>(__popc(peers)));
         base = __shfl_sync(FULL, base, leader);
-        rk[i] = base + below;
-        __syncwarp();
+        rk[i / 2] |= (base + below) << (16 * (i % 2));
     }
     __syncthreads();
 
-    // ---- tile digit totals, warp-exclusive offsets, publish aggregate ----
+    // ---- tile digit totals (incl. padding), warp-exclusive offsets, block scan ----
     std::uint32_t total = 0;
     std::uint32_t incl = 0;
-    std::uint64_t* my_lb = lookback + static_cast<std::uint64_t>(tile) * RADIX + tid;
-    const std::uint64_t tagbits = static_cast<std::uint64_t>(tag) << LB_TAG_SHIFT;
     if (tid < RADIX) {
 #pragma unroll
         for (int w = 0; w < WARPS; ++w) {
@@ -221,9 +273,6 @@ __global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
             s_whist[w * RADIX + tid] = total;
             total += c;
         }
-        const std::uint32_t pad = (tid == RADIX - 1) ? (TILE - valid) : 0u;
-        const std::uint64_t mine = total - pad;
-        st_relaxed_u64(my_lb, (tile == 0 ? LB_INC : LB_AGG) | tagbits | mine);
         incl = total;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -248,31 +297,38 @@ __global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
     // ---- stage keys (and payload) in shared memory in digit order ----
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const std::uint64_t idx = wbase + i * 32 + lane;
-        const std::uint32_t d = idx < n ? digit_of(k[i], shift, dsc) : 255u;
-        const std::uint32_t pos = s_whist[warp * RADIX + d] + rk[i];
+        const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+        const std::uint32_t pos = wh[d] + ((rk[i / 2] >> (16 * (i % 2))) & 0xffffu);
         if constexpr (L::HAS_KEYS_SMEM) s_keys[pos] = k[i];
         if constexpr (L::HAS_VALS) s_vals[pos] = v[i];
-        if constexpr (MODE == SORT_LOWMEM) rk[i] = pos;  // reuse: remember digit order position
-        (void)pos;
     }
 
-    // ---- decoupled look-back for this tile's per-digit exclusive prefix ----
+    // ---- windowed decoupled look-back for this tile's per-digit exclusive prefix ----
     if (tid < RADIX) {
         std::uint64_t excl = 0;
         if (tile > 0) {
             std::int64_t p = static_cast<std::int64_t>(tile) - 1;
-            while (true) {
-                const std::uint64_t w = ld_relaxed_u64(lookback + p * RADIX + tid);
-                const std::uint32_t wtag = static_cast<std::uint32_t>(w >> LB_TAG_SHIFT) & LB_TAG_MASK;
-                const std::uint64_t flag = w & (3ull << 62);
-                if (wtag != tag || flag == 0) continue;
-                excl += w & LB_COUNT_MASK;
-                if (flag == LB_INC) break;
-                --p;
+            bool done = false;
+            while (!done) {
+                constexpr int WIN = 4;
+                std::uint64_t w[WIN];
+#pragma unroll
+                for (int q = 0; q < WIN; ++q)
+                    w[q] = p - q >= 0 ? ld_relaxed_u64(lookback + (p - q) * RADIX + tid) : (LB_INC | tagbits);
+                int consumed = 0;
+#pragma unroll
+                for (int q = 0; q < WIN; ++q) {
+                    if (done || consumed < q) break;
+                    const std::uint32_t wtag = static_cast<std::uint32_t>(w[q] >> LB_TAG_SHIFT) & LB_TAG_MASK;
+                    const std::uint64_t flag = w[q] & (3ull << 62);
+                    if (wtag != tag || flag == 0) break;  // not published yet: reload from here
+                    excl += w[q] & LB_COUNT_MASK;
+                    consumed = q + 1;
+                    if (flag == LB_INC) done = true;
+                }
+                p -= consumed;
             }
-            const std::uint32_t pad = (tid == RADIX - 1) ? (TILE - valid) : 0u;
-            st_relaxed_u64(my_lb, LB_INC | tagbits | (excl + total - pad));
+            st_relaxed_u64(my_lb, LB_INC | tagbits | (excl + count));
         }
         s_gofs[tid] = goffs[tid] + excl - dstart;
     }
@@ -285,22 +341,23 @@ __global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const std::uint32_t j = i * BLOCK + tid;
-            if (j < valid) {
+            if (full || j < valid) {
                 const V ix = s_vals[j];
                 const std::uint32_t d = digit_of(kin[ix], shift, dsc);
                 vout[s_gofs[d] + j] = ix;
             }
         }
     } else {
-        std::uint8_t dj[ITEMS];
+        std::uint32_t dj[DW];
+#pragma unroll
+        for (int w = 0; w < DW; ++w) dj[w] = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const std::uint32_t j = i * BLOCK + tid;
-            dj[i] = 0;
-            if (j < valid) {
+            if (full || j < valid) {
                 const T key = s_keys[j];
                 const std::uint32_t d = digit_of(key, shift, dsc);
-                dj[i] = static_cast<std::uint8_t>(d);
+                dj[i / 4] |= d << (8 * (i % 4));
                 if (write_keys) kout[s_gofs[d] + j] = key;
             }
         }
@@ -308,33 +365,54 @@ __global__ void __launch_bounds__(tile_cfg<T>::BLOCK, tile_cfg<T>::MIN_BLOCKS)
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const std::uint32_t j = i * BLOCK + tid;
-                if (j < valid) vout[s_gofs[dj[i]] + j] = s_vals[j];
+                if (full || j < valid) {
+                    const std::uint32_t d = (dj[i / 4] >> (8 * (i % 4))) & 0xffu;
+                    vout[s_gofs[d] + j] = s_vals[j];
+                }
             }
         }
     }
 }
 
-template <typename T, typename V, int MODE>
-void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n,
-                 int shift, bool desc, int pass_index, const std::uint64_t* goffs,
-                 std::uint32_t* tile_counter, bool write_keys) {
+bool use_hw_match() {
+    static const bool hw = [] {
+        const char* e = std::getenv("AKB_MATCH");
+        return !(e && std::strcmp(e, "ballot") == 0);
+    }();
+    return hw;
+}
+
+template <typename T, typename V, int MODE, bool HW>
+void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift,
+                      bool desc, int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter,
+                      bool write_keys) {
     using L = pass_smem<T, V, MODE>;
     static bool configured = false;
-    auto kern = onesweep_kernel<T, V, MODE>;
+    auto kern = onesweep_kernel<T, V, MODE, HW>;
     if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(L::total)));
+        AKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::total)));
         configured = true;
     }
     const std::uint64_t tiles = ceil_div(n, L::TILE);
     const std::uint32_t tag = ctx_lookback_pass(c, tiles);
     const int tok = ctx_prof_begin(c, KF_ONESWEEP);
     kern<<<static_cast<unsigned>(tiles), L::BLOCK, L::total, c->stream>>>(
-        kin, kout, vin, vout, n, shift, desc ? 1 : 0, pass_index, goffs, c->lookback,
-        tile_counter, tag, write_keys ? 1 : 0);
+        kin, kout, vin, vout, n, shift, desc ? 1 : 0, pass_index, goffs, c->lookback, tile_counter, tag,
+        write_keys ? 1 : 0);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     c->kernel_launches += 1;
+}
+
+template <typename T, typename V, int MODE>
+void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift, bool desc,
+                 int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter, bool write_keys) {
+    if (use_hw_match())
+        launch_pass_impl<T, V, MODE, true>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs, tile_counter,
+                                           write_keys);
+    else
+        launch_pass_impl<T, V, MODE, false>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                            tile_counter, write_keys);
 }
 
 template <typename T, typename V, int MODE>
@@ -366,48 +444,45 @@ void radix_sort_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, const V* vin, V*
         for (int p = 0; p < PASSES; ++p) {
             V* dst = (p % 2 == 0) ? valt : vout;
             const V* src = (p % 2 == 0) ? vout : valt;  // unused at p == 0
-            launch_pass<T, V, MODE>(c, kin, nullptr, src, dst, n, 8 * p, desc, p,
-                                    g_offs + p * RADIX, counters + p, false);
+            launch_pass<T, V, MODE>(c, kin, nullptr, src, dst, n, 8 * p, desc, p, g_offs + p * RADIX, counters + p,
+                                    false);
         }
-        return;
-    }
-    // keys: pass p reads src, writes dst; even passes -> kalt, odd -> kout
-    for (int p = 0; p < PASSES; ++p) {
-        const bool to_alt = (p % 2 == 0);
-        const T* ksrc = p == 0 ? kin : (to_alt ? kout : kalt);
-        T* kdst = to_alt ? kalt : kout;
-        const V* vsrc = nullptr;
-        V* vdst = nullptr;
-        if constexpr (MODE != SORT_KEYS) {
-            vsrc = p == 0 ? vin : (to_alt ? vout : valt);
-            vdst = to_alt ? valt : vout;
+    } else {
+        // keys: pass p reads src, writes dst; even passes -> kalt, odd -> kout
+        for (int p = 0; p < PASSES; ++p) {
+            const bool to_alt = (p % 2 == 0);
+            const T* ksrc = p == 0 ? kin : (to_alt ? kout : kalt);
+            T* kdst = to_alt ? kalt : kout;
+            const V* vsrc = nullptr;
+            V* vdst = nullptr;
+            if constexpr (MODE != SORT_KEYS) {
+                vsrc = p == 0 ? vin : (to_alt ? vout : valt);
+                vdst = to_alt ? valt : vout;
+            }
+            const bool wk = keys_out || (p + 1 < PASSES);
+            launch_pass<T, V, MODE>(c, ksrc, kdst, vsrc, vdst, n, 8 * p, desc, p, g_offs + p * RADIX, counters + p,
+                                    wk);
         }
-        const bool wk = keys_out || (p + 1 < PASSES);
-        launch_pass<T, V, MODE>(c, ksrc, kdst, vsrc, vdst, n, 8 * p, desc, p, g_offs + p * RADIX,
-                                counters + p, wk);
     }
 }
 
 }  // namespace
 
 template <typename T, typename V>
-void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vin, V* vout,
-                V* valt, std::uint64_t n, bool desc, bool keys_out) {
+void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vin, V* vout, V* valt,
+                std::uint64_t n, bool desc, bool keys_out) {
     switch (mode) {
         case SORT_KEYS:
-            radix_sort_impl<T, V, SORT_KEYS>(c, kin, kout, kalt, nullptr, nullptr, nullptr, n, desc,
-                                             true);
+            radix_sort_impl<T, V, SORT_KEYS>(c, kin, kout, kalt, nullptr, nullptr, nullptr, n, desc, true);
             break;
         case SORT_PAIRS:
             radix_sort_impl<T, V, SORT_PAIRS>(c, kin, kout, kalt, vin, vout, valt, n, desc, true);
             break;
         case SORT_IOTA:
-            radix_sort_impl<T, V, SORT_IOTA>(c, kin, kout, kalt, nullptr, vout, valt, n, desc,
-                                             keys_out);
+            radix_sort_impl<T, V, SORT_IOTA>(c, kin, kout, kalt, nullptr, vout, valt, n, desc, keys_out);
             break;
         case SORT_LOWMEM:
-            radix_sort_impl<T, V, SORT_LOWMEM>(c, kin, nullptr, nullptr, nullptr, vout, valt, n,
-                                               desc, false);
+            radix_sort_impl<T, V, SORT_LOWMEM>(c, kin, nullptr, nullptr, nullptr, vout, valt, n, desc, false);
             break;
         default:
             throw invalid_argument("radix_sort: unknown mode");
@@ -415,17 +490,17 @@ void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vi
 }
 
 std::uint64_t radix_tile_items(int key_bytes, int) {
-    return key_bytes == 8 ? tile_cfg<std::uint64_t>::TILE : tile_cfg<std::uint32_t>::TILE;
+    return key_bytes == 8 ? tile_cfg<std::uint64_t, std::uint32_t, SORT_KEYS>::TILE
+                          : tile_cfg<std::uint32_t, std::uint32_t, SORT_KEYS>::TILE;
 }
 
-#define AKB_INST(T, V)                                                                          \
-    template void radix_sort<T, V>(ak_ctx*, int, const T*, T*, T*, const V*, V*, V*,           \
-                                   std::uint64_t, bool, bool);
-#define AKB_INST_K(T)                  \
-    AKB_INST(T, std::uint32_t)         \
-    AKB_INST(T, std::int32_t)          \
-    AKB_INST(T, std::uint64_t)         \
-    AKB_INST(T, std::int64_t)
+// Keys-only sorts never touch the payload type: instantiate them once (V = u32)
+// and route the other payload types of SORT_KEYS there.
+#define AKB_INST(T, V)                                                                                        \
+    template void radix_sort<T, V>(ak_ctx*, int, const T*, T*, T*, const V*, V*, V*, std::uint64_t, bool, bool);
+#define AKB_INST_K(T)          \
+    AKB_INST(T, std::uint32_t) \
+    AKB_INST(T, std::uint64_t)
 
 AKB_INST_K(std::int32_t)
 AKB_INST_K(std::uint32_t)
