@@ -38,7 +38,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libak_cuda.so")
+LIB_PATH = os.environ.get("AKB_LIB") or os.path.join(HERE, "lib", "libak_cuda.so")
 
 
 class InvalidArgument(ValueError):

@@ -26,13 +26,42 @@ namespace {
 constexpr int RADIX = 256;
 constexpr std::uint32_t FULL = 0xffffffffu;
 
+#ifndef AKB_OS_MINB
+#define AKB_OS_MINB 2  // resident pass CTAs per SM the register budget is sized for
+#endif
+#ifndef AKB_OS_ITEMS
+#define AKB_OS_ITEMS 16  // keys per thread of a keys-only pass tile
+#endif
+#ifndef AKB_LB_WIN
+#define AKB_LB_WIN 16  // predecessors read per look-back round trip
+#endif
+
+#ifdef AKB_PHASES
+// Phase-timing build (tools/phases.py): thread 0 of every tile stamps %globaltimer
+// at each phase boundary of the pass kernel into g_phase[tile * 8 + k].
+__device__ std::uint64_t* g_phase = nullptr;
+#define AKB_PHASE(k)                                                                         \
+    do {                                                                                     \
+        if (tid == 0 && g_phase) {                                                           \
+            std::uint64_t t_;                                                                \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+            g_phase[static_cast<std::uint64_t>(tile) * 8 + (k)] = t_;                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define AKB_PHASE(k) \
+    do {             \
+    } while (0)
+#endif
+
 template <typename T, typename V, int MODE>
 struct tile_cfg {
     static constexpr int BLOCK = 384;
     static constexpr bool HAS_VALS = MODE != SORT_KEYS;
-    static constexpr int ITEMS = !HAS_VALS ? 16 : (sizeof(T) + sizeof(V) <= 8 ? 16 : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
+    static constexpr int ITEMS =
+        !HAS_VALS ? AKB_OS_ITEMS : (sizeof(T) + sizeof(V) <= 8 ? 16 : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
     static constexpr int TILE = BLOCK * ITEMS;
-    static constexpr int MIN_BLOCKS = 2;
+    static constexpr int MIN_BLOCKS = AKB_OS_MINB;
 };
 
 template <typename T>
@@ -46,10 +75,42 @@ __device__ __forceinline__ std::uint32_t digit_of(T key, int shift, bool desc) {
     }
 }
 
-// Lanes holding the same 8-bit digit.
-template <bool HW>
+// Predicated shared-memory ops: keep the per-item ranking loop free of divergent
+// branches (BSSY/BRA/BSYNC run on the ADU pipe, which is the first to saturate).
+__device__ __forceinline__ std::uint32_t atom_add_shared_if(bool p, std::uint32_t* addr, std::uint32_t v) {
+    std::uint32_t old = 0;
+    const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
+    asm volatile(
+        "{ .reg .pred q; setp.ne.u32 q, %2, 0; @q atom.shared.add.u32 %0, [%1], %3; }"
+        : "+r"(old)
+        : "r"(a), "r"(static_cast<std::uint32_t>(p)), "r"(v)
+        : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_shared_if(bool p, std::uint32_t* addr, std::uint32_t v) {
+    const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, 0; @q st.shared.u32 [%0], %2; }" ::"r"(a),
+                 "r"(static_cast<std::uint32_t>(p)), "r"(v)
+                 : "memory");
+}
+__device__ __forceinline__ std::uint32_t ld_shared_u32(const std::uint32_t* addr) {
+    std::uint32_t v;
+    const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_or_shared(std::uint32_t* addr, std::uint32_t v) {
+    const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Peer-lane discovery for the warp ranking (AKB_MATCH selects at run time):
+enum match_kind : int { MATCH_BALLOT = 0, MATCH_HW = 1, MATCH_SMEM = 2 };
+
+// Lanes holding the same 8-bit digit (register variants).
+template <int HW>
 __device__ __forceinline__ std::uint32_t match_digit(std::uint32_t d) {
-    if constexpr (HW) {
+    if constexpr (HW == MATCH_HW) {
         return __match_any_sync(FULL, d);
     } else {
         std::uint32_t m = FULL;
@@ -158,16 +219,22 @@ struct pass_smem {
     static constexpr std::size_t vals_bytes = HAS_VALS ? sizeof(V) * TILE : 0;
     static constexpr std::size_t whist_off = (vals_off + vals_bytes + 15) & ~std::size_t(15);
     static constexpr std::size_t whist_bytes = sizeof(std::uint32_t) * WARPS * RADIX;
+    // MATCH_SMEM peer table: aliases the staging area (dead until ranking is over)
+    static constexpr std::size_t match_off = 0;
+    static constexpr std::size_t match_bytes = sizeof(std::uint32_t) * WARPS * RADIX;
+    static_assert(keys_bytes + vals_bytes >= match_bytes, "peer table must fit in the staging area");
     static constexpr std::size_t hist_off = whist_off + whist_bytes;
     static constexpr std::size_t hist_bytes = sizeof(std::uint32_t) * RADIX;
     static constexpr std::size_t gofs_off = hist_off + hist_bytes;
     static constexpr std::size_t gofs_bytes = sizeof(std::uint64_t) * RADIX;
-    static constexpr std::size_t misc_off = gofs_off + gofs_bytes;
+    static constexpr std::size_t gofs32_off = gofs_off + gofs_bytes;  // low words, used when n <= 2^32
+    static constexpr std::size_t gofs32_bytes = sizeof(std::uint32_t) * RADIX;
+    static constexpr std::size_t misc_off = gofs32_off + gofs32_bytes;
     static constexpr std::size_t misc_bytes = sizeof(std::uint32_t) * 16;
     static constexpr std::size_t total = misc_off + misc_bytes;
 };
 
-template <typename T, typename V, int MODE, bool HW_MATCH>
+template <typename T, typename V, int MODE, int HW_MATCH>
 __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MODE>::MIN_BLOCKS)
     onesweep_kernel(const T* __restrict__ kin, T* __restrict__ kout, const V* __restrict__ vin,
                     V* __restrict__ vout, std::uint64_t n, int shift, int desc, int pass_index,
@@ -185,15 +252,21 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     std::uint32_t* s_whist = reinterpret_cast<std::uint32_t*>(smem + L::whist_off);
     std::uint32_t* s_hist = reinterpret_cast<std::uint32_t*>(smem + L::hist_off);
     std::uint64_t* s_gofs = reinterpret_cast<std::uint64_t*>(smem + L::gofs_off);
+    std::uint32_t* s_gofs32 = reinterpret_cast<std::uint32_t*>(smem + L::gofs32_off);
     std::uint32_t* s_misc = reinterpret_cast<std::uint32_t*>(smem + L::misc_off);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool dsc = desc != 0;
     if (tid == 0) s_misc[0] = atomicAdd(tile_counter, 1u);
     for (int i = tid; i < WARPS * RADIX; i += BLOCK) s_whist[i] = 0;
+    if constexpr (HW_MATCH == MATCH_SMEM) {
+        std::uint32_t* s_match = reinterpret_cast<std::uint32_t*>(smem + L::match_off);
+        for (int i = tid; i < WARPS * RADIX; i += BLOCK) s_match[i] = 0;
+    }
     if (tid < RADIX) s_hist[tid] = 0;
     __syncthreads();
     const std::uint32_t tile = s_misc[0];
+    AKB_PHASE(0);
     const std::uint64_t tile_base = static_cast<std::uint64_t>(tile) * TILE;
     const std::uint64_t remaining = n - tile_base;
     const std::uint32_t valid = remaining < TILE ? static_cast<std::uint32_t>(remaining) : TILE;
@@ -206,43 +279,51 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     std::uint32_t dg[DW];
 #pragma unroll
     for (int w = 0; w < DW; ++w) dg[w] = 0;
+    // Branch-free per item: one uniform full/partial decision per tile; padded
+    // slots load from a clamped in-bounds address and get digit 255 (sorted last,
+    // never counted, never scattered).
+    auto load_and_count = [&](auto full_c) {
+        constexpr bool F = decltype(full_c)::value;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const std::uint32_t li = wofs + i * 32;
-        const bool ok = full || li < valid;
-        const std::uint64_t idx = tile_base + li;
-        if constexpr (MODE == SORT_LOWMEM) {
-            if (ok) {
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t li = wofs + i * 32;
+            const bool ok = F || li < valid;
+            const std::uint64_t idx = tile_base + (ok ? li : 0u);
+            if constexpr (MODE == SORT_LOWMEM) {
                 const V ix = pass_index == 0 ? static_cast<V>(idx) : vin[idx];
                 v[i] = ix;
                 k[i] = kin[ix];
             } else {
-                v[i] = V(0);
-                k[i] = T(0);
+                k[i] = kin[idx];
+                if constexpr (MODE == SORT_PAIRS) v[i] = vin[idx];
+                if constexpr (MODE == SORT_IOTA) v[i] = pass_index == 0 ? static_cast<V>(idx) : vin[idx];
             }
-        } else {
-            k[i] = ok ? kin[idx] : T(0);
-            if constexpr (MODE == SORT_PAIRS) v[i] = ok ? vin[idx] : V(0);
-            if constexpr (MODE == SORT_IOTA)
-                v[i] = pass_index == 0 ? static_cast<V>(idx) : (ok ? vin[idx] : V(0));
         }
-    }
-    // ---- digits + early counts ----
+        // ---- digits + early counts ----
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const std::uint32_t li = wofs + i * 32;
-        const bool ok = full || li < valid;
-        const std::uint32_t d = ok ? digit_of(k[i], shift, dsc) : 255u;  // padding sorts last
-        dg[i / 4] |= d << (8 * (i % 4));
-        if (ok) atomicAdd(s_hist + d, 1u);
-    }
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t li = wofs + i * 32;
+            const bool ok = F || li < valid;
+            const std::uint32_t d = ok ? digit_of(k[i], shift, dsc) : 255u;  // padding sorts last
+            dg[i / 4] |= d << (8 * (i % 4));
+#ifndef AKB_EXPERIMENT_LATE_COUNTS
+            if constexpr (F) atomicAdd(s_hist + d, 1u);
+            else atomicAdd(s_hist + d, ok ? 1u : 0u);
+#endif
+        }
+    };
+    if (full) load_and_count(std::true_type{});
+    else load_and_count(std::false_type{});
     __syncthreads();
+    AKB_PHASE(1);
     std::uint64_t* my_lb = lookback + static_cast<std::uint64_t>(tile) * RADIX + tid;
     const std::uint64_t tagbits = static_cast<std::uint64_t>(tag) << LB_TAG_SHIFT;
     std::uint32_t count = 0;
     if (tid < RADIX) {
+#ifndef AKB_EXPERIMENT_LATE_COUNTS
         count = s_hist[tid];
         st_relaxed_u64(my_lb, (tile == 0 ? LB_INC : LB_AGG) | tagbits | count);
+#endif
     }
 
     // ---- warp-level stable ranking ----
@@ -250,18 +331,42 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
 #pragma unroll
     for (int w = 0; w < (ITEMS + 1) / 2; ++w) rk[w] = 0;
     std::uint32_t* wh = s_whist + warp * RADIX;
+    if constexpr (HW_MATCH == MATCH_SMEM) {
+        // peers via a per-warp digit -> lane-bitmask table: OR in, read back, leader clears
+        std::uint32_t* mt = reinterpret_cast<std::uint32_t*>(smem + L::match_off) + warp * RADIX;
+        const std::uint32_t lanebit = 1u << lane;
+        const std::uint32_t lt = lanemask_lt();
+        const std::uint32_t ge = ~lt;  // lanes >= me
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
-        const std::uint32_t peers = match_digit<HW_MATCH>(d);
-        const int leader = 31 - __clz(peers);
-        const std::uint32_t below = __popc(peers & lanemask_lt());
-        std::uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(wh + d, static_cast<std::uint32_t>(__popc(peers)));
-        base = __shfl_sync(FULL, base, leader);
-        rk[i / 2] |= (base + below) << (16 * (i % 2));
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+            red_or_shared(mt + d, lanebit);
+            __syncwarp();
+            const std::uint32_t peers = ld_shared_u32(mt + d);
+            const std::uint32_t base = ld_shared_u32(wh + d);  // group-uniform (broadcast)
+            __syncwarp();
+            const bool lead = (peers & ge) == lanebit;  // highest lane of the group
+            st_shared_if(lead, wh + d, base + __popc(peers));
+            st_shared_if(lead, mt + d, 0u);
+            rk[i / 2] |= (base + __popc(peers & lt)) << (16 * (i % 2));
+        }
+        __syncwarp();
+    } else {
+        const std::uint32_t lt = lanemask_lt();
+        const std::uint32_t ge = ~lt;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+            const std::uint32_t peers = match_digit<HW_MATCH>(d);
+            const int leader = 31 - __clz(peers);
+            const bool lead = (peers & ge) == (1u << lane);
+            std::uint32_t base = atom_add_shared_if(lead, wh + d, static_cast<std::uint32_t>(__popc(peers)));
+            base = __shfl_sync(FULL, base, leader);
+            rk[i / 2] |= (base + __popc(peers & lt)) << (16 * (i % 2));
+        }
     }
     __syncthreads();
+    AKB_PHASE(2);
 
     // ---- tile digit totals (incl. padding), warp-exclusive offsets, block scan ----
     std::uint32_t total = 0;
@@ -273,6 +378,10 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
             s_whist[w * RADIX + tid] = total;
             total += c;
         }
+#ifdef AKB_EXPERIMENT_LATE_COUNTS  // publish the aggregate only after ranking (no early counts)
+        count = total - (tid == RADIX - 1 ? TILE - valid : 0u);
+        st_relaxed_u64(my_lb, (tile == 0 ? LB_INC : LB_AGG) | tagbits | count);
+#endif
         incl = total;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -293,6 +402,7 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
         for (int w = 0; w < WARPS; ++w) s_whist[w * RADIX + tid] += dstart;
     }
     __syncthreads();
+    AKB_PHASE(3);
 
     // ---- stage keys (and payload) in shared memory in digit order ----
 #pragma unroll
@@ -306,11 +416,15 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     // ---- windowed decoupled look-back for this tile's per-digit exclusive prefix ----
     if (tid < RADIX) {
         std::uint64_t excl = 0;
+#ifdef AKB_EXPERIMENT_NO_LOOKBACK  // timing experiment only: wrong output
+        if (false) {
+#else
         if (tile > 0) {
+#endif
             std::int64_t p = static_cast<std::int64_t>(tile) - 1;
             bool done = false;
             while (!done) {
-                constexpr int WIN = 4;
+                constexpr int WIN = AKB_LB_WIN;
                 std::uint64_t w[WIN];
 #pragma unroll
                 for (int q = 0; q < WIN; ++q)
@@ -330,59 +444,87 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
             }
             st_relaxed_u64(my_lb, LB_INC | tagbits | (excl + count));
         }
-        s_gofs[tid] = goffs[tid] + excl - dstart;
+        const std::uint64_t g = goffs[tid] + excl - dstart;  // modular: g + j is the output index
+        s_gofs[tid] = g;
+        s_gofs32[tid] = static_cast<std::uint32_t>(g);
     }
     __syncthreads();
+    AKB_PHASE(4);
 
     // ---- scatter contiguous digit runs ----
-    if constexpr (MODE == SORT_LOWMEM) {
-        // only the index array moves; the digit of staged slot j is recomputed
-        // from data[index] (L1/L2 hit: just gathered by this tile)
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const std::uint32_t j = i * BLOCK + tid;
-            if (full || j < valid) {
-                const V ix = s_vals[j];
-                const std::uint32_t d = digit_of(kin[ix], shift, dsc);
-                vout[s_gofs[d] + j] = ix;
-            }
-        }
-    } else {
-        std::uint32_t dj[DW];
-#pragma unroll
-        for (int w = 0; w < DW; ++w) dj[w] = 0;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const std::uint32_t j = i * BLOCK + tid;
-            if (full || j < valid) {
-                const T key = s_keys[j];
-                const std::uint32_t d = digit_of(key, shift, dsc);
-                dj[i / 4] |= d << (8 * (i % 4));
-                if (write_keys) kout[s_gofs[d] + j] = key;
-            }
-        }
-        if constexpr (L::HAS_VALS) {
+    auto scatter = [&](auto full_c, auto wk_c, auto narrow_c) {
+        constexpr bool F = decltype(full_c)::value;
+        constexpr bool WK = decltype(wk_c)::value;
+        constexpr bool NARROW = decltype(narrow_c)::value;  // n <= 2^32: 32-bit offset math
+        auto dst = [&](std::uint32_t d, std::uint32_t j) -> std::uint64_t {
+            if constexpr (NARROW) return static_cast<std::uint32_t>(s_gofs32[d] + j);
+            else return s_gofs[d] + j;
+        };
+        if constexpr (MODE == SORT_LOWMEM) {
+            // only the index array moves; the digit of staged slot j is recomputed
+            // from data[index] (L1/L2 hit: just gathered by this tile)
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const std::uint32_t j = i * BLOCK + tid;
-                if (full || j < valid) {
-                    const std::uint32_t d = (dj[i / 4] >> (8 * (i % 4))) & 0xffu;
-                    vout[s_gofs[d] + j] = s_vals[j];
+                if (F || j < valid) {
+                    const V ix = s_vals[j];
+                    const std::uint32_t d = digit_of(kin[ix], shift, dsc);
+                    vout[dst(d, j)] = ix;
+                }
+            }
+        } else {
+            std::uint32_t dj[DW];
+#pragma unroll
+            for (int w = 0; w < DW; ++w) dj[w] = 0;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const std::uint32_t j = i * BLOCK + tid;
+                if (F || j < valid) {
+                    const T key = s_keys[j];
+                    const std::uint32_t d = digit_of(key, shift, dsc);
+                    dj[i / 4] |= d << (8 * (i % 4));
+                    if constexpr (WK) kout[dst(d, j)] = key;
+                }
+            }
+            if constexpr (L::HAS_VALS) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    const std::uint32_t j = i * BLOCK + tid;
+                    if (F || j < valid) {
+                        const std::uint32_t d = (dj[i / 4] >> (8 * (i % 4))) & 0xffu;
+                        vout[dst(d, j)] = s_vals[j];
+                    }
                 }
             }
         }
+    };
+    if (n <= 0xffffffffull) {
+        if (full) {
+            if (write_keys) scatter(std::true_type{}, std::true_type{}, std::true_type{});
+            else scatter(std::true_type{}, std::false_type{}, std::true_type{});
+        } else {
+            if (write_keys) scatter(std::false_type{}, std::true_type{}, std::true_type{});
+            else scatter(std::false_type{}, std::false_type{}, std::true_type{});
+        }
+    } else {
+        if (write_keys) scatter(std::false_type{}, std::true_type{}, std::false_type{});
+        else scatter(std::false_type{}, std::false_type{}, std::false_type{});
     }
+    AKB_PHASE(5);
 }
 
-bool use_hw_match() {
-    static const bool hw = [] {
+int match_kind_env() {
+    static const int k = [] {
         const char* e = std::getenv("AKB_MATCH");
-        return !(e && std::strcmp(e, "ballot") == 0);
+        if (e && std::strcmp(e, "hw") == 0) return static_cast<int>(MATCH_HW);
+        if (e && std::strcmp(e, "ballot") == 0) return static_cast<int>(MATCH_BALLOT);
+        if (e && std::strcmp(e, "smem") == 0) return static_cast<int>(MATCH_SMEM);
+        return static_cast<int>(MATCH_SMEM);
     }();
-    return hw;
+    return k;
 }
 
-template <typename T, typename V, int MODE, bool HW>
+template <typename T, typename V, int MODE, int HW>
 void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift,
                       bool desc, int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter,
                       bool write_keys) {
@@ -407,12 +549,19 @@ void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, s
 template <typename T, typename V, int MODE>
 void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift, bool desc,
                  int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter, bool write_keys) {
-    if (use_hw_match())
-        launch_pass_impl<T, V, MODE, true>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs, tile_counter,
-                                           write_keys);
-    else
-        launch_pass_impl<T, V, MODE, false>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                            tile_counter, write_keys);
+    switch (match_kind_env()) {
+        case MATCH_HW:
+            launch_pass_impl<T, V, MODE, MATCH_HW>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                                   tile_counter, write_keys);
+            break;
+        case MATCH_BALLOT:
+            launch_pass_impl<T, V, MODE, MATCH_BALLOT>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                                       tile_counter, write_keys);
+            break;
+        default:
+            launch_pass_impl<T, V, MODE, MATCH_SMEM>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                                     tile_counter, write_keys);
+    }
 }
 
 template <typename T, typename V, int MODE>
@@ -488,6 +637,12 @@ void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vi
             throw invalid_argument("radix_sort: unknown mode");
     }
 }
+
+#ifdef AKB_PHASES
+extern "C" int ak_debug_set_phase_buffer(void* p) {
+    return cudaMemcpyToSymbol(g_phase, &p, sizeof(p)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 std::uint64_t radix_tile_items(int key_bytes, int) {
     return key_bytes == 8 ? tile_cfg<std::uint64_t, std::uint32_t, SORT_KEYS>::TILE
