@@ -139,6 +139,16 @@ __device__ __forceinline__ void st_release_u32(std::uint32_t* p, std::uint32_t v
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// 16-byte look-back descriptors {value bits, status word}: one aligned 128-bit
+// access, so a reader sees value and status from the same publication without a
+// release/acquire pair (which compile to MEMBAR.ALL.GPU / CCTL.IVALL on sm_100a).
+__device__ __forceinline__ void st_relaxed_desc(std::uint64_t* p, std::uint64_t value, std::uint64_t status) {
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(value), "l"(status) : "memory");
+}
+__device__ __forceinline__ void ld_relaxed_desc(const std::uint64_t* p, std::uint64_t& value, std::uint64_t& status) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(value), "=l"(status) : "l"(p) : "memory");
+}
+
 inline std::uint64_t ceil_div(std::uint64_t a, std::uint64_t b) { return (a + b - 1) / b; }
 
 }  // namespace akb

@@ -66,8 +66,7 @@ std::uint32_t ctx_scan_pass(ak_ctx* c, std::size_t tiles) {
         clear = true;
     }
     if (clear) {
-        AKB_CUDA(cudaMemsetAsync(c->scan_flags, 0, c->scan_tiles * sizeof(std::uint32_t),
-                                 c->stream));
+        AKB_CUDA(cudaMemsetAsync(c->scan_vals, 0, 2 * c->scan_tiles * sizeof(std::uint64_t), c->stream));
     }
     return c->scan_epoch;
 }

@@ -35,9 +35,9 @@ struct ak_ctx {
     std::size_t lookback_words = 0;
     std::uint32_t lb_epoch = 0;
 
-    // scan look-back: per tile flag word (epoch tagged) + two 64-bit values
-    std::uint32_t* scan_flags = nullptr;
-    std::uint64_t* scan_vals = nullptr;  // [2 * tiles]: aggregate, inclusive
+    // scan look-back: one 16-byte descriptor per tile {value bits, status | tag}
+    std::uint32_t* scan_flags = nullptr;  // unused (kept for layout stability)
+    std::uint64_t* scan_vals = nullptr;   // [2 * tiles]
     std::size_t scan_tiles = 0;
     std::uint32_t scan_epoch = 0;
 

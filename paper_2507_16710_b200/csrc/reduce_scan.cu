@@ -164,58 +164,94 @@ __global__ void __launch_bounds__(RED_BLOCK)
 }
 
 // ---------------------------------------------------------------------------
-// K2: single-pass scan, dynamic tiles, warp-cooperative decoupled look-back.
-// Tile = 256 threads x ITEMS; warp w owns a contiguous run of 32*ITEMS
-// elements processed in rounds of 32 (coalesced, one element per lane).
+// K2: single-pass scan, dynamic tiles, decoupled look-back (Merrill & Garland;
+// the "opportunistic look-back" of PAPER.md:161).
+//   load   : coalesced 16-byte loads, transposed through a padded shared tile
+//            (one pad element per 16 -> conflict-free blocked reads);
+//   local  : each thread scans its 16 contiguous elements serially, warp shuffle
+//            scan of thread totals, block scan of 8 warp totals;
+//   chain  : warp 0 publishes the tile aggregate, looks back 32 tiles per round
+//            trip, publishes the inclusive prefix;
+//   store  : results back through the same shared slots, coalesced 16-byte stores.
+// Floats accumulate in double (acc_of), so carries over ~2^18 tiles stay exact
+// enough for the 1e-5 contract.
 // ---------------------------------------------------------------------------
 constexpr int SCAN_BLOCK = 256;
 
 template <typename T>
 struct scan_cfg {
-    static constexpr int ITEMS = sizeof(T) == 8 ? 16 : 24;
+    static constexpr int ITEMS = 16;
     static constexpr int TILE = SCAN_BLOCK * ITEMS;
+    static constexpr int PADDED = TILE + TILE / ITEMS;  // one pad slot per thread run
+    static constexpr int VEC = 16 / sizeof(T);
 };
 
-template <typename T, int OP>
-__global__ void __launch_bounds__(SCAN_BLOCK)
+__device__ __forceinline__ int scan_slot(int e) { return e + (e >> 4); }
+
+template <typename T, int OP, bool VECIO>
+__global__ void __launch_bounds__(SCAN_BLOCK, 4)
     scan_kernel(const T* x, T* out, std::uint64_t n, T init, int inclusive, std::uint32_t* flags,
                 std::uint64_t* vals, std::uint32_t tag, std::uint32_t* tile_counter) {
     using A = typename acc_of<T>::type;
     using F = opf<A, OP>;
-    constexpr int ITEMS = scan_cfg<T>::ITEMS;
-    constexpr int TILE = scan_cfg<T>::TILE;
+    using Cfg = scan_cfg<T>;
+    constexpr int ITEMS = Cfg::ITEMS;
+    constexpr int TILE = Cfg::TILE;
+    constexpr int VEC = Cfg::VEC;
     constexpr int WARPS = SCAN_BLOCK / 32;
+    __shared__ __align__(16) T s_tile[Cfg::PADDED];
     __shared__ A s_warp[WARPS];
     __shared__ A s_excl;
-    __shared__ std::uint32_t s_tile;
+    __shared__ std::uint32_t s_tile_id;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    if (tid == 0) s_tile_id = atomicAdd(tile_counter, 1u);
     __syncthreads();
-    const std::uint32_t tile = s_tile;
-    const std::uint64_t wbase =
-        static_cast<std::uint64_t>(tile) * TILE + static_cast<std::uint64_t>(warp) * 32 * ITEMS;
+    const std::uint32_t tile = s_tile_id;
+    const std::uint64_t base = static_cast<std::uint64_t>(tile) * TILE;
+    const std::uint64_t rem = n - base;
+    const bool full = rem >= static_cast<std::uint64_t>(TILE);
 
-    A v[ITEMS];
+    // ---- load: global (coalesced) -> padded shared tile ----
+    if (VECIO && full) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + base);
+        uint4 q[TILE / VEC / SCAN_BLOCK];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const std::uint64_t idx = wbase + i * 32 + lane;
-        v[i] = idx < n ? static_cast<A>(x[idx]) : F::identity();
-    }
-    // inclusive scan of the warp's run; v[i] becomes the run-local inclusive prefix
-    A carry = F::identity();
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) q[j] = __ldg(src + j * SCAN_BLOCK + tid);
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        A s = v[i];
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) {
+            const T* e = reinterpret_cast<const T*>(&q[j]);
+            const int e0 = (j * SCAN_BLOCK + tid) * VEC;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const A y = shfl_up_any(s, o);
-            if (lane >= o) s = F::apply(y, s);
+            for (int k = 0; k < VEC; ++k) s_tile[scan_slot(e0 + k)] = e[k];
         }
-        s = F::apply(carry, s);
-        v[i] = s;
-        carry = shfl_any(s, 31);
+    } else {
+#pragma unroll 4
+        for (int e = tid; e < TILE; e += SCAN_BLOCK)
+            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot(e)] = x[base + e];
     }
-    if (lane == 0) s_warp[warp] = carry;
+    __syncthreads();
+
+    // ---- thread-serial scan of 16 contiguous elements ----
+    const int my0 = tid * ITEMS;
+    A v[ITEMS];
+    A run = F::identity();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool ok = full || static_cast<std::uint64_t>(my0 + i) < rem;
+        const A xi = ok ? static_cast<A>(s_tile[scan_slot(my0 + i)]) : F::identity();
+        run = F::apply(run, xi);
+        v[i] = run;  // thread-local inclusive prefix
+    }
+    // warp scan of thread totals
+    A winc = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const A y = shfl_up_any(winc, o);
+        if (lane >= o) winc = F::apply(y, winc);
+    }
+    A texcl = shfl_up_any(winc, 1);  // exclusive prefix of this thread within its warp
+    if (lane == 0) texcl = F::identity();
+    if (lane == 31) s_warp[warp] = winc;
     __syncthreads();
     A wexcl = F::identity();
     A tile_total = F::identity();
@@ -225,70 +261,93 @@ __global__ void __launch_bounds__(SCAN_BLOCK)
         tile_total = F::apply(tile_total, s_warp[w]);
     }
 
+    // ---- decoupled look-back (warp 0). Descriptor per tile, published with one
+    // relaxed store: 4-byte accumulators pack {status|tag : value} into one 64-bit
+    // word; 8-byte accumulators use two such words (one per 32-bit value half),
+    // stored together and accepted only when both halves carry the same status,
+    // so correctness needs only 64-bit single-copy atomicity ----
     if (warp == 0) {
         A excl = F::identity();
+        constexpr bool NARROW = sizeof(A) == 4;
+        std::uint64_t* my = vals + (NARROW ? 1 : 2) * static_cast<std::uint64_t>(tile);
+        auto publish = [&](A v, std::uint32_t status) {
+            const std::uint64_t b = to_bits(v);
+            const std::uint64_t hi_status = static_cast<std::uint64_t>(status) << 32;
+            if constexpr (NARROW) st_relaxed_u64(my, hi_status | b);
+            else st_relaxed_desc(my, hi_status | (b & 0xffffffffull), hi_status | (b >> 32));
+        };
         if (tile == 0) {
-            if (lane == 0) {
-                st_relaxed_u64(vals + 1, to_bits(tile_total));
-                st_release_u32(flags, SC_INC | tag);
-            }
+            if (lane == 0) publish(tile_total, SC_INC | tag);
         } else {
-            if (lane == 0) {
-                st_relaxed_u64(vals + 2 * static_cast<std::uint64_t>(tile), to_bits(tile_total));
-                st_release_u32(flags + tile, SC_AGG | tag);
-            }
-            std::int64_t base = static_cast<std::int64_t>(tile) - 1;
+            if (lane == 0) publish(tile_total, SC_AGG | tag);
+            std::int64_t pbase = static_cast<std::int64_t>(tile) - 1;
             while (true) {
-                const std::int64_t p = base - lane;
-                std::uint32_t f = SC_INC;
-                bool ready = true;
+                const std::int64_t p = pbase - lane;
+                std::uint64_t vb = 0;
+                std::uint32_t f = SC_INC | tag;
                 if (p >= 0) {
-                    f = ld_acquire_u32(flags + p);
-                    ready = (f & SC_TAG_MASK) == tag && (f & ~SC_TAG_MASK) != 0;
+                    if constexpr (NARROW) {
+                        const std::uint64_t w = ld_relaxed_u64(vals + p);
+                        vb = w & 0xffffffffull;
+                        f = static_cast<std::uint32_t>(w >> 32);
+                    } else {
+                        // each 64-bit half carries the status word; a read that straddles a
+                        // republication sees two different statuses and is treated as not ready
+                        std::uint64_t w0, w1;
+                        ld_relaxed_desc(vals + 2 * static_cast<std::uint64_t>(p), w0, w1);
+                        vb = (w0 & 0xffffffffull) | (w1 << 32);
+                        const std::uint32_t f0 = static_cast<std::uint32_t>(w0 >> 32);
+                        f = f0 == static_cast<std::uint32_t>(w1 >> 32) ? f0 : 0u;
+                    }
                 }
+                const bool ready = (f & SC_TAG_MASK) == tag && (f & ~SC_TAG_MASK) != 0;
                 const std::uint32_t ready_mask = __ballot_sync(FULL, ready);
-                const std::uint32_t inc_mask =
-                    __ballot_sync(FULL, ready && (p < 0 || (f & ~SC_TAG_MASK) == SC_INC));
+                const std::uint32_t inc_mask = __ballot_sync(FULL, ready && (f & ~SC_TAG_MASK) == SC_INC);
                 const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
                 const int first_nr = ~ready_mask ? __ffs(~ready_mask) - 1 : 32;
                 if (first_nr <= first_inc && first_nr < 32) continue;  // a needed tile is not published yet
                 const int lim = first_inc < 32 ? first_inc : 31;
-                A a = F::identity();
-                if (p >= 0 && lane <= lim) {
-                    const bool inc = (lane == lim) && inc_mask;
-                    a = from_bits<A>(ld_relaxed_u64(vals + 2 * static_cast<std::uint64_t>(p) + (inc ? 1 : 0)));
-                }
-                // fold in order nearest-last: reduce lanes lim..0 (commutative ops)
+                A a = (p >= 0 && lane <= lim) ? from_bits<A>(vb) : F::identity();
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) a = F::apply(a, shfl_xor_any(a, o));
                 excl = F::apply(a, excl);
                 if (inc_mask) break;
-                base -= 32;
+                pbase -= 32;
             }
-            if (lane == 0) {
-                st_relaxed_u64(vals + 2 * static_cast<std::uint64_t>(tile) + 1,
-                               to_bits(F::apply(excl, tile_total)));
-                st_release_u32(flags + tile, SC_INC | tag);
-            }
+            if (lane == 0) publish(F::apply(excl, tile_total), SC_INC | tag);
         }
         if (lane == 0) s_excl = excl;
     }
     __syncthreads();
-    const A pre = F::apply(F::apply(static_cast<A>(init), s_excl), wexcl);
-    A prev_carry = F::identity();
+
+    // ---- results back into this thread's own shared slots ----
+    const A pre = F::apply(F::apply(F::apply(static_cast<A>(init), s_excl), wexcl), texcl);
+    if (inclusive) {
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const std::uint64_t idx = wbase + i * 32 + lane;
-        A r;
-        if (inclusive) {
-            r = F::apply(pre, v[i]);
-        } else {
-            A up = shfl_up_any(v[i], 1);
-            if (lane == 0) up = prev_carry;
-            r = (i == 0 && lane == 0) ? pre : F::apply(pre, up);
-            prev_carry = shfl_any(v[i], 31);
+        for (int i = 0; i < ITEMS; ++i) s_tile[scan_slot(my0 + i)] = static_cast<T>(F::apply(pre, v[i]));
+    } else {
+        s_tile[scan_slot(my0)] = static_cast<T>(pre);
+#pragma unroll
+        for (int i = 1; i < ITEMS; ++i) s_tile[scan_slot(my0 + i)] = static_cast<T>(F::apply(pre, v[i - 1]));
+    }
+    __syncthreads();
+
+    // ---- store: padded shared tile -> global (coalesced) ----
+    if (VECIO && full) {
+        uint4* dst = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) {
+            uint4 q;
+            T* e = reinterpret_cast<T*>(&q);
+            const int e0 = (j * SCAN_BLOCK + tid) * VEC;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) e[k] = s_tile[scan_slot(e0 + k)];
+            dst[j * SCAN_BLOCK + tid] = q;
         }
-        if (idx < n) out[idx] = static_cast<T>(r);
+    } else {
+#pragma unroll 4
+        for (int e = tid; e < TILE; e += SCAN_BLOCK)
+            if (static_cast<std::uint64_t>(e) < rem) out[base + e] = s_tile[scan_slot(e)];
     }
 }
 
@@ -336,12 +395,19 @@ void scan(ak_ctx* c, const T* x, T* out, std::uint64_t n, int op, int inclusive,
     std::uint32_t* counter = reinterpret_cast<std::uint32_t*>(static_cast<char*>(c->small) + 131072);
     AKB_CUDA(cudaMemsetAsync(counter, 0, 4, c->stream));
     const int tok = ctx_prof_begin(c, KF_SCAN);
-#define AKB_SCAN(OPV)                                                                          \
-    scan_kernel<T, OPV><<<static_cast<unsigned>(tiles), SCAN_BLOCK, 0, c->stream>>>(            \
+    const bool vecio = ((reinterpret_cast<std::uintptr_t>(x) | reinterpret_cast<std::uintptr_t>(out)) & 15) == 0;
+#define AKB_SCAN(OPV, V)                                                                       \
+    scan_kernel<T, OPV, V><<<static_cast<unsigned>(tiles), SCAN_BLOCK, 0, c->stream>>>(         \
         x, out, n, init, inclusive, c->scan_flags, c->scan_vals, tag, counter)
-    if (op == OP_SUM) AKB_SCAN(OP_SUM);
-    else if (op == OP_MIN) AKB_SCAN(OP_MIN);
-    else AKB_SCAN(OP_MAX);
+    if (vecio) {
+        if (op == OP_SUM) AKB_SCAN(OP_SUM, true);
+        else if (op == OP_MIN) AKB_SCAN(OP_MIN, true);
+        else AKB_SCAN(OP_MAX, true);
+    } else {
+        if (op == OP_SUM) AKB_SCAN(OP_SUM, false);
+        else if (op == OP_MIN) AKB_SCAN(OP_MIN, false);
+        else AKB_SCAN(OP_MAX, false);
+    }
 #undef AKB_SCAN
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
