@@ -163,6 +163,18 @@ typedef int (*ak_exchange_fn)(void* user, const void* send_base, const uint64_t*
                               const uint64_t* recv_cnt, uint64_t elem_bytes);
 int ak_comm_callbacks_create(int nranks, int rank, void* user, ak_allgather_fn ag,
                              ak_allreduce_u64_fn ar, ak_exchange_fn ex, ak_comm** out);
+/* sim::world + rank_comm (sim_comm.hpp:41-181) on ONE device: P logical ranks, each driven
+ * by its own host thread and ak_ctx; collectives are host-level, slices move device to
+ * device. abort() wakes every blocked rank with AK_ETRANSPORT (sim_comm.cpp:19-25). */
+typedef struct ak_world ak_world;
+int ak_world_create(int ranks, ak_world** out);
+int ak_world_size(const ak_world* w);
+int ak_world_abort(ak_world* w);
+int ak_world_destroy(ak_world* w);
+int ak_comm_loopback_create(ak_world* w, int rank, ak_comm** out);
+/* 1 when p is device (or managed) memory, else 0: the C++ headers run host spans through
+ * HBM staging and device spans in place */
+int ak_pointer_is_device(const void* p);
 int ak_comm_rank(const ak_comm* comm);
 int ak_comm_size(const ak_comm* comm);
 int ak_comm_allreduce_sum_u64(ak_comm* comm, ak_ctx* ctx, uint64_t* host_inout, uint64_t n);

@@ -18,7 +18,14 @@
 
 struct ak_comm {
     std::unique_ptr<akb::comm_iface> impl;
-    akb::nccl_comm* nccl = nullptr;  // non-owning view when impl is NCCL
+    akb::nccl_comm* nccl = nullptr;      // non-owning view when impl is NCCL
+    akb::loopback_comm* loop = nullptr;  // non-owning view when impl is a loopback rank
+};
+
+// sim::world (sim_comm.hpp:41-80) on one device: P logical ranks, one host thread each.
+struct ak_world {
+    akb::loopback_world w;
+    explicit ak_world(int ranks) : w(ranks) {}
 };
 
 namespace {
@@ -221,6 +228,7 @@ void search_impl(ak_ctx* c, const T* hay, std::uint64_t n, const T* needles, std
 akb::comm_iface& comm_of(ak_comm* comm, self_comm& fallback, ak_ctx* c) {
     if (!comm) return fallback;
     if (comm->nccl) comm->nccl->stream = c->stream;
+    if (comm->loop) comm->loop->stream = c->stream;
     return *comm->impl;
 }
 
@@ -559,6 +567,49 @@ int ak_comm_callbacks_create(int nranks, int rank, void* user, ak_allgather_fn a
         c->impl = std::make_unique<akb::callback_comm>(rank, nranks, user, ag, ar, ex);
         *out = c.release();
     });
+}
+
+int ak_world_create(int ranks, ak_world** out) {
+    return guard([&] {
+        need(out != nullptr, "ak_world_create: null output");
+        need(ranks >= 1, "world: rank count must be >= 1");  // sim_comm.cpp:7-9
+        *out = new ak_world(ranks);
+    });
+}
+
+int ak_world_size(const ak_world* w) { return w ? w->w.P : 0; }
+
+int ak_world_abort(ak_world* w) {
+    return guard([&] {
+        need(w != nullptr, "ak_world_abort: null world");
+        w->w.abort();
+    });
+}
+
+int ak_world_destroy(ak_world* w) {
+    return guard([&] { delete w; });
+}
+
+int ak_comm_loopback_create(ak_world* w, int rank, ak_comm** out) {
+    return guard([&] {
+        need(w && out, "ak_comm_loopback_create: null argument");
+        need(rank >= 0 && rank < w->w.P, "rank_comm: rank out of range");  // sim_comm.cpp:11-13
+        auto impl = std::make_unique<akb::loopback_comm>(&w->w, rank, nullptr);
+        auto c = std::make_unique<ak_comm>();
+        c->loop = impl.get();
+        c->impl = std::move(impl);
+        *out = c.release();
+    });
+}
+
+int ak_pointer_is_device(const void* p) {
+    if (!p) return 0;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 1 : 0;
 }
 
 int ak_comm_rank(const ak_comm* c) { return c ? c->impl->rank() : 0; }
