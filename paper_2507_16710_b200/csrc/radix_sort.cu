@@ -32,8 +32,20 @@ constexpr std::uint32_t FULL = 0xffffffffu;
 #ifndef AKB_OS_ITEMS
 #define AKB_OS_ITEMS 16  // keys per thread of a keys-only pass tile
 #endif
+#ifndef AKB_OS_BLOCK
+#define AKB_OS_BLOCK 384  // threads per pass CTA (>= RADIX)
+#endif
+#ifndef AKB_HYB_K
+#define AKB_HYB_K 3  // MATCH_HYBRID: every K-th item ranks by ballots, the rest by the peer table
+#endif
 #ifndef AKB_LB_WIN
-#define AKB_LB_WIN 16  // predecessors read per look-back round trip
+#define AKB_LB_WIN 4  // predecessors read per look-back round trip (r01 sweep: 2/4/8/16 -> 4 best)
+#endif
+// Tile counts are published to the look-back chain right after ranking (from the
+// per-warp histograms the ranking builds anyway) instead of with a separate early
+// shared-atomic count: one shared atomic per key less (r01: -5.5% per pass).
+#ifndef AKB_EARLY_COUNTS
+#define AKB_EXPERIMENT_LATE_COUNTS
 #endif
 
 #ifdef AKB_PHASES
@@ -56,7 +68,7 @@ __device__ std::uint64_t* g_phase = nullptr;
 
 template <typename T, typename V, int MODE>
 struct tile_cfg {
-    static constexpr int BLOCK = 384;
+    static constexpr int BLOCK = AKB_OS_BLOCK;
     static constexpr bool HAS_VALS = MODE != SORT_KEYS;
     static constexpr int ITEMS =
         !HAS_VALS ? AKB_OS_ITEMS : (sizeof(T) + sizeof(V) <= 8 ? 16 : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
@@ -105,7 +117,7 @@ __device__ __forceinline__ void red_or_shared(std::uint32_t* addr, std::uint32_t
 }
 
 // Peer-lane discovery for the warp ranking (AKB_MATCH selects at run time):
-enum match_kind : int { MATCH_BALLOT = 0, MATCH_HW = 1, MATCH_SMEM = 2 };
+enum match_kind : int { MATCH_BALLOT = 0, MATCH_HW = 1, MATCH_SMEM = 2, MATCH_HYBRID = 3, MATCH_HALF = 4 };
 
 // Lanes holding the same 8-bit digit (register variants).
 template <int HW>
@@ -217,12 +229,15 @@ struct pass_smem {
     static constexpr std::size_t keys_bytes = HAS_KEYS_SMEM ? sizeof(T) * TILE : 0;
     static constexpr std::size_t vals_off = keys_off + keys_bytes;
     static constexpr std::size_t vals_bytes = HAS_VALS ? sizeof(V) * TILE : 0;
-    static constexpr std::size_t whist_off = (vals_off + vals_bytes + 15) & ~std::size_t(15);
-    static constexpr std::size_t whist_bytes = sizeof(std::uint32_t) * WARPS * RADIX;
-    // MATCH_SMEM peer table: aliases the staging area (dead until ranking is over)
+    // MATCH_SMEM peer tables (two for MATCH_SMEM2): alias the staging area, which is dead
+    // until ranking is over
     static constexpr std::size_t match_off = 0;
     static constexpr std::size_t match_bytes = sizeof(std::uint32_t) * WARPS * RADIX;
-    static_assert(keys_bytes + vals_bytes >= match_bytes, "peer table must fit in the staging area");
+    static constexpr std::size_t stage_bytes =
+        keys_bytes + vals_bytes > 2 * match_bytes ? keys_bytes + vals_bytes : 2 * match_bytes;
+    static constexpr std::size_t whist_off = (stage_bytes + 15) & ~std::size_t(15);
+    // per ranking group (warp, or half-warp for MATCH_HALF) running digit counts
+    static constexpr std::size_t whist_bytes = sizeof(std::uint32_t) * 2 * WARPS * RADIX;
     static constexpr std::size_t hist_off = whist_off + whist_bytes;
     static constexpr std::size_t hist_bytes = sizeof(std::uint32_t) * RADIX;
     static constexpr std::size_t gofs_off = hist_off + hist_bytes;
@@ -256,12 +271,20 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     std::uint32_t* s_misc = reinterpret_cast<std::uint32_t*>(smem + L::misc_off);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // ranking groups: warps, or half-warps (MATCH_HALF: 16 lanes, each group owning a
+    // contiguous run of 16*ITEMS keys, count and peer mask packed in one shared word)
+    constexpr bool HALF = HW_MATCH == MATCH_HALF;
+    constexpr int VW = HALF ? 2 * WARPS : WARPS;
+    constexpr int GL = HALF ? 16 : 32;
+    const int vw = HALF ? warp * 2 + (lane >> 4) : warp;
+    const int gl = HALF ? (lane & 15) : lane;
     const bool dsc = desc != 0;
     if (tid == 0) s_misc[0] = atomicAdd(tile_counter, 1u);
-    for (int i = tid; i < WARPS * RADIX; i += BLOCK) s_whist[i] = 0;
-    if constexpr (HW_MATCH == MATCH_SMEM) {
+    for (int i = tid; i < VW * RADIX; i += BLOCK) s_whist[i] = 0;
+    if constexpr (HW_MATCH == MATCH_SMEM || HW_MATCH == MATCH_HYBRID) {
         std::uint32_t* s_match = reinterpret_cast<std::uint32_t*>(smem + L::match_off);
-        for (int i = tid; i < WARPS * RADIX; i += BLOCK) s_match[i] = 0;
+        constexpr int TABLES = 1;
+        for (int i = tid; i < TABLES * WARPS * RADIX; i += BLOCK) s_match[i] = 0;
     }
     if (tid < RADIX) s_hist[tid] = 0;
     __syncthreads();
@@ -271,7 +294,7 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     const std::uint64_t remaining = n - tile_base;
     const std::uint32_t valid = remaining < TILE ? static_cast<std::uint32_t>(remaining) : TILE;
     const bool full = valid == TILE;
-    const std::uint32_t wofs = static_cast<std::uint32_t>(warp) * 32 * ITEMS + lane;  // tile-local index of item 0
+    const std::uint32_t wofs = static_cast<std::uint32_t>(vw) * GL * ITEMS + gl;  // tile-local index of item 0
 
     // ---- load (warp-striped: item i of lane l is tile-local wofs + 32 i) ----
     T k[ITEMS];
@@ -286,7 +309,7 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
         constexpr bool F = decltype(full_c)::value;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const std::uint32_t li = wofs + i * 32;
+            const std::uint32_t li = wofs + i * GL;
             const bool ok = F || li < valid;
             const std::uint64_t idx = tile_base + (ok ? li : 0u);
             if constexpr (MODE == SORT_LOWMEM) {
@@ -302,7 +325,7 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
         // ---- digits + early counts ----
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const std::uint32_t li = wofs + i * 32;
+            const std::uint32_t li = wofs + i * GL;
             const bool ok = F || li < valid;
             const std::uint32_t d = ok ? digit_of(k[i], shift, dsc) : 255u;  // padding sorts last
             dg[i / 4] |= d << (8 * (i % 4));
@@ -330,8 +353,56 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     std::uint32_t rk[(ITEMS + 1) / 2];  // warp-local ranks (< 32*ITEMS), two 16-bit per word
 #pragma unroll
     for (int w = 0; w < (ITEMS + 1) / 2; ++w) rk[w] = 0;
-    std::uint32_t* wh = s_whist + warp * RADIX;
-    if constexpr (HW_MATCH == MATCH_SMEM) {
+    std::uint32_t* wh = s_whist + vw * RADIX;
+    if constexpr (HALF) {
+        // word = running count << 16 | peer mask of this item (16 lanes)
+        const std::uint32_t bit = 1u << gl;
+        const std::uint32_t lt16 = bit - 1u;
+        const std::uint32_t ge16 = 0xffffu & ~lt16;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+            red_or_shared(wh + d, bit);
+            __syncwarp();
+            const std::uint32_t w = ld_shared_u32(wh + d);
+            __syncwarp();
+            const std::uint32_t peers = w & 0xffffu, base = w >> 16;
+            const bool lead = (peers & ge16) == bit;  // highest lane of the group
+            st_shared_if(lead, wh + d, (base + __popc(peers)) << 16);
+            rk[i / 2] |= (base + __popc(peers & lt16)) << (16 * (i % 2));
+        }
+        __syncwarp();
+    } else if constexpr (HW_MATCH == MATCH_HYBRID) {
+        // Split the peer discovery between two pipes: every AKB_HYB_K-th item finds its
+        // peers with 8 ballots (ALU/vote), the others through the shared peer table
+        // (LSU). Both read and bump the same per-warp running digit counts.
+        std::uint32_t* mt = reinterpret_cast<std::uint32_t*>(smem + L::match_off) + warp * RADIX;
+        const std::uint32_t lanebit = 1u << lane;
+        const std::uint32_t lt = lanemask_lt();
+        const std::uint32_t ge = ~lt;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+            constexpr int K = AKB_HYB_K;
+            const bool by_vote = (i % K) == K - 1;
+            std::uint32_t peers;
+            if (by_vote) {
+                peers = match_digit<MATCH_BALLOT>(d);
+                __syncwarp();
+            } else {
+                red_or_shared(mt + d, lanebit);
+                __syncwarp();
+                peers = ld_shared_u32(mt + d);
+            }
+            const std::uint32_t base = ld_shared_u32(wh + d);
+            __syncwarp();
+            const bool lead = (peers & ge) == lanebit;
+            st_shared_if(lead, wh + d, base + __popc(peers));
+            if (!by_vote) st_shared_if(lead, mt + d, 0u);
+            rk[i / 2] |= (base + __popc(peers & lt)) << (16 * (i % 2));
+        }
+        __syncwarp();
+    } else if constexpr (HW_MATCH == MATCH_SMEM) {
         // peers via a per-warp digit -> lane-bitmask table: OR in, read back, leader clears
         std::uint32_t* mt = reinterpret_cast<std::uint32_t*>(smem + L::match_off) + warp * RADIX;
         const std::uint32_t lanebit = 1u << lane;
@@ -373,8 +444,8 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     std::uint32_t incl = 0;
     if (tid < RADIX) {
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) {
-            const std::uint32_t c = s_whist[w * RADIX + tid];
+        for (int w = 0; w < VW; ++w) {
+            const std::uint32_t c = HALF ? (s_whist[w * RADIX + tid] >> 16) : s_whist[w * RADIX + tid];
             s_whist[w * RADIX + tid] = total;
             total += c;
         }
@@ -399,7 +470,7 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
             if (w < warp) wp += s_misc[4 + w];
         dstart = wp + incl - total;
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) s_whist[w * RADIX + tid] += dstart;
+        for (int w = 0; w < VW; ++w) s_whist[w * RADIX + tid] += dstart;
     }
     __syncthreads();
     AKB_PHASE(3);
@@ -519,7 +590,9 @@ int match_kind_env() {
         if (e && std::strcmp(e, "hw") == 0) return static_cast<int>(MATCH_HW);
         if (e && std::strcmp(e, "ballot") == 0) return static_cast<int>(MATCH_BALLOT);
         if (e && std::strcmp(e, "smem") == 0) return static_cast<int>(MATCH_SMEM);
-        return static_cast<int>(MATCH_SMEM);
+        if (e && std::strcmp(e, "hybrid") == 0) return static_cast<int>(MATCH_HYBRID);
+        if (e && std::strcmp(e, "half") == 0) return static_cast<int>(MATCH_HALF);
+        return static_cast<int>(MATCH_HALF);  // r01 sweep: half 12.97 / hybrid 13.12 / smem 13.35 / ballot 14.5 / hw 18.6 ms
     }();
     return k;
 }
@@ -557,6 +630,14 @@ void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::u
         case MATCH_BALLOT:
             launch_pass_impl<T, V, MODE, MATCH_BALLOT>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
                                                        tile_counter, write_keys);
+            break;
+        case MATCH_HALF:
+            launch_pass_impl<T, V, MODE, MATCH_HALF>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                                     tile_counter, write_keys);
+            break;
+        case MATCH_HYBRID:
+            launch_pass_impl<T, V, MODE, MATCH_HYBRID>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                                      tile_counter, write_keys);
             break;
         default:
             launch_pass_impl<T, V, MODE, MATCH_SMEM>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
