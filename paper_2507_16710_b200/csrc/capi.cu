@@ -361,6 +361,7 @@ int ak_ctx_destroy(ak_ctx* c) {
         if (c->scan_vals) cudaFree(c->scan_vals);
         if (c->small) cudaFree(c->small);
         if (c->split) cudaFree(c->split);
+        if (c->cuts) cudaFree(c->cuts);
         if (c->stage) cudaFree(c->stage);
         if (c->pinned) cudaFreeHost(c->pinned);
         for (auto& t : c->pending) {
@@ -407,7 +408,7 @@ int ak_ctx_set_profiling(ak_ctx* c, int on) {
 int ak_ctx_kernel_time(ak_ctx* c, int family, double* ms, uint64_t* launches) {
     return guard([&] {
         ctx_lock g(c);
-        need(family >= 0 && family < 8, "ak_ctx_kernel_time: bad family");
+        need(family >= 0 && family < 9, "ak_ctx_kernel_time: bad family");
         AKB_CUDA(cudaStreamSynchronize(c->stream));
         akb::ctx_prof_resolve(c);
         if (ms) *ms = c->family_ms[family];
@@ -420,7 +421,7 @@ int ak_ctx_reset_kernel_time(ak_ctx* c) {
         ctx_lock g(c);
         AKB_CUDA(cudaStreamSynchronize(c->stream));
         akb::ctx_prof_resolve(c);
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 16; ++i) {
             c->family_ms[i] = 0;
             c->family_count[i] = 0;
         }

@@ -135,6 +135,19 @@ void* ctx_stage(ak_ctx* c, std::size_t bytes) {
     return c->stage;
 }
 
+std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count) {
+    if (count > c->cuts_cap) {
+        if (c->cuts) {
+            AKB_CUDA(cudaStreamSynchronize(c->stream));
+            AKB_CUDA(cudaFree(c->cuts));
+        }
+        std::size_t grow = count < 4096 ? 4096 : count + count / 2;
+        AKB_CUDA(cudaMalloc(&c->cuts, grow * sizeof(std::uint64_t)));
+        c->cuts_cap = grow;
+    }
+    return c->cuts;
+}
+
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count) {
     if (count > c->split_cap) {
         if (c->split) {

@@ -49,6 +49,10 @@ struct ak_ctx {
     std::uint64_t* split = nullptr;
     std::size_t split_cap = 0;
 
+    // hybrid radix sort: range cut points + oversized-range list
+    std::uint64_t* cuts = nullptr;
+    std::size_t cuts_cap = 0;
+
     // device staging for the *_host entry points (end-to-end path)
     void* stage = nullptr;
     std::size_t stage_bytes = 0;
@@ -68,8 +72,8 @@ struct ak_ctx {
     };
     std::vector<timed> pending;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
-    double family_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    std::uint64_t family_count[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double family_ms[16] = {};
+    std::uint64_t family_count[16] = {};
 };
 
 namespace akb {
@@ -95,11 +99,12 @@ std::uint32_t ctx_scan_pass(ak_ctx* c, std::size_t tiles);
 void ctx_finish(ak_ctx* c);  // synchronise when blocking
 void* ctx_pinned(ak_ctx* c, std::size_t bytes);
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count);
+std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count);
 void* ctx_stage(ak_ctx* c, std::size_t bytes);
 
 // Kernel families for ak_ctx_kernel_time (C ABI: AK_KF_*).
 enum kernel_family : int { KF_ONESWEEP = 0, KF_HIST = 1, KF_MERGE = 2, KF_REDUCE = 3, KF_SCAN = 4,
-                           KF_SEARCH = 5, KF_EXCHANGE = 6, KF_OTHER = 7 };
+                           KF_SEARCH = 5, KF_EXCHANGE = 6, KF_OTHER = 7, KF_LOCAL = 8 };
 // Bracket one launch with events when profiling is on (returns -1 when off).
 int ctx_prof_begin(ak_ctx* c, int family);
 void ctx_prof_end(ak_ctx* c, int token);

@@ -13,9 +13,11 @@
 //   5. windowed decoupled look-back (4 predecessors in flight per digit) ->
 //      INC publish and global digit bases;
 //   6. scatter contiguous per-digit runs.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "radix_sort.cuh"
 
@@ -111,6 +113,21 @@ __device__ __forceinline__ std::uint32_t ld_shared_u32(const std::uint32_t* addr
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
+__device__ __forceinline__ void red_or_shared_if(bool p, std::uint32_t* addr, std::uint32_t v) {
+    const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q red.shared.or.b32 [%0], %1; }" ::"r"(a), "r"(v),
+                 "r"(static_cast<std::uint32_t>(p))
+                 : "memory");
+}
+__device__ __forceinline__ std::uint32_t ld_shared_u32_if(bool p, const std::uint32_t* addr) {
+    std::uint32_t v = 0;
+    const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.shared.u32 %0, [%1]; }"
+                 : "+r"(v)
+                 : "r"(a), "r"(static_cast<std::uint32_t>(p))
+                 : "memory");
+    return v;
+}
 __device__ __forceinline__ void red_or_shared(std::uint32_t* addr, std::uint32_t v) {
     const std::uint32_t a = static_cast<std::uint32_t>(__cvta_generic_to_shared(addr));
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -141,20 +158,22 @@ __device__ __forceinline__ std::uint32_t match_digit(std::uint32_t d) {
 // Upfront histogram: one read of the keys, all D digit histograms.
 // PARTS sub-histograms per digit spread same-digit lanes over banks.
 // ---------------------------------------------------------------------------
-template <typename T, int PASSES>
+// Digits [FIRST, PASSES) are counted (the hybrid sort only needs its top digits).
+template <typename T, int PASSES, int FIRST = 0>
 __global__ void __launch_bounds__(256) hist_kernel(const T* __restrict__ keys, std::uint64_t n,
                                                    int desc, std::uint64_t* __restrict__ g_hist) {
     constexpr int PARTS = 4;
-    __shared__ std::uint32_t sh[PASSES * RADIX * PARTS];
-    for (int i = threadIdx.x; i < PASSES * RADIX * PARTS; i += blockDim.x) sh[i] = 0;
+    constexpr int CNT = PASSES - FIRST;
+    __shared__ std::uint32_t sh[CNT * RADIX * PARTS];
+    for (int i = threadIdx.x; i < CNT * RADIX * PARTS; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     const int part = threadIdx.x % PARTS;
     auto count = [&](T k) {
         const auto o = ordered(k, desc != 0);
 #pragma unroll
-        for (int p = 0; p < PASSES; ++p) {
+        for (int p = FIRST; p < PASSES; ++p) {
             const std::uint32_t d = static_cast<std::uint32_t>((o >> (8 * p)) & 0xffu);
-            atomicAdd(&sh[(p * RADIX + d) * PARTS + part], 1u);
+            atomicAdd(&sh[((p - FIRST) * RADIX + d) * PARTS + part], 1u);
         }
     };
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
@@ -187,11 +206,13 @@ __global__ void __launch_bounds__(256) hist_kernel(const T* __restrict__ keys, s
     }
     for (std::uint64_t i = done + tid; i < n; i += stride) count(keys[i]);
     __syncthreads();
-    for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) {
+    for (int i = threadIdx.x; i < CNT * RADIX; i += blockDim.x) {
         std::uint32_t s = 0;
 #pragma unroll
         for (int q = 0; q < PARTS; ++q) s += sh[i * PARTS + q];
-        if (s) atomicAdd(reinterpret_cast<unsigned long long*>(g_hist + i), static_cast<unsigned long long>(s));
+        if (s)
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_hist + FIRST * RADIX + i),
+                      static_cast<unsigned long long>(s));
     }
 }
 
@@ -696,6 +717,381 @@ void radix_sort_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, const V* vin, V*
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Hybrid MSD/LSD sort (keys only).
+//   1. m global onesweep passes over the TOP m digits (LSD order among them) leave the
+//      array stably ordered by its top 8m bits ("buckets");
+//   2. the array is cut at bucket starts into ranges of at most LOCAL_TILE keys
+//      (cut j = start of the bucket holding position j*step);
+//   3. one CTA per range sorts it completely on chip: keys stay in registers, each
+//      local pass ranks them (half-warp peer/count words, as the global pass) and
+//      exchanges them through shared memory; only digits that vary inside the range
+//      are passed over (the range's top digits are usually constant).
+// Every key in range j precedes every key in range j+1 (cuts sit on bucket starts), equal
+// keys share a bucket, and every pass is stable, so the result equals the stable LSD sort
+// (= the reference's stable merge sort). Ranges that do not fit (skewed keys) are sorted
+// afterwards by the plain onesweep LSD on their segment. Global traffic: m passes + one
+// read and one write, instead of D passes.
+// ---------------------------------------------------------------------------
+constexpr int LOCAL_BLOCK = 384;
+constexpr int LOCAL_MAX_ITEMS = 16;
+constexpr int LOCAL_TILE = LOCAL_BLOCK * LOCAL_MAX_ITEMS;  // 6144 keys per range at most
+constexpr int LOCAL_VW = LOCAL_BLOCK / 16;                  // half-warp ranking groups
+constexpr int LOCAL_WARPS = LOCAL_BLOCK / 32;
+
+template <typename T, int ITEMS>
+struct local_smem {
+    static constexpr std::size_t stage_off = 0;
+    static constexpr std::size_t stage_bytes = sizeof(T) * LOCAL_BLOCK * ITEMS;
+    static constexpr std::size_t tab_off = stage_bytes;
+    static constexpr std::size_t tab_bytes = sizeof(std::uint32_t) * LOCAL_VW * RADIX;
+    static constexpr std::size_t wsum_off = tab_off + tab_bytes;  // 8 x u32 digit-scan warp sums
+    static constexpr std::size_t red_off = wsum_off + 64;          // 2 x WARPS x u64 or/and partials
+    static constexpr std::size_t total = red_off + 2 * LOCAL_WARPS * sizeof(std::uint64_t);
+};
+
+template <typename T, int ITEMS>
+__global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3 : 2))
+    local_sort_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
+                      int desc, std::uint64_t* big) {
+    using L = local_smem<T, ITEMS>;
+    using B = typename key_traits<T>::bits;
+    constexpr int CAP = LOCAL_BLOCK * ITEMS;
+    constexpr int PASSES = key_traits<T>::nbits / 8;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* s_stage = reinterpret_cast<T*>(smem + L::stage_off);
+    std::uint32_t* s_tab = reinterpret_cast<std::uint32_t*>(smem + L::tab_off);
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    B* s_red = reinterpret_cast<B*>(smem + L::red_off);
+
+    const std::uint64_t b = cuts[blockIdx.x], e = cuts[blockIdx.x + 1];
+    if (b >= e) return;
+    if (e - b > static_cast<std::uint64_t>(CAP)) {  // left for the segment fallback
+        if (threadIdx.x == 0) {
+            const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+            big[1 + slot] = blockIdx.x;
+        }
+        return;
+    }
+    const std::uint32_t len = static_cast<std::uint32_t>(e - b);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int vw = warp * 2 + (lane >> 4), gl = lane & 15;
+    const std::uint32_t base_i = static_cast<std::uint32_t>(vw) * 16 * ITEMS + gl;  // item i at base_i + 16 i
+    const bool dsc = desc != 0;
+
+    T k[ITEMS];
+    B orv = 0, andv = static_cast<B>(~B(0));
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint32_t li = base_i + 16 * i;
+        const bool ok = li < len;
+        k[i] = in[b + (ok ? li : 0u)];
+        const B o = ordered(k[i], dsc);
+        orv |= ok ? o : B(0);
+        andv &= ok ? o : static_cast<B>(~B(0));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        orv |= __shfl_xor_sync(FULL, orv, o);
+        andv &= __shfl_xor_sync(FULL, andv, o);
+    }
+    if (lane == 0) {
+        s_red[warp] = orv;
+        s_red[LOCAL_WARPS + warp] = andv;
+    }
+    __syncthreads();
+    B any1 = 0, all1 = static_cast<B>(~B(0));
+#pragma unroll
+    for (int w = 0; w < LOCAL_WARPS; ++w) {
+        any1 |= s_red[w];
+        all1 &= s_red[LOCAL_WARPS + w];
+    }
+    const B vary = any1 & ~all1;  // bits that differ between keys of this range
+
+    std::uint32_t* wh = s_tab + vw * RADIX;
+    const std::uint32_t bit = 1u << gl;
+    const std::uint32_t lt16 = bit - 1u;
+    const std::uint32_t ge16 = 0xffffu & ~lt16;
+#pragma unroll 1
+    for (int p = 0; p < PASSES; ++p) {
+        const std::uint32_t vmask = static_cast<std::uint32_t>(vary >> (8 * p)) & 0xffu;
+        if (vmask == 0) continue;  // block-uniform
+        // Narrow digits (<= 8 distinct values in this range, e.g. the bucket digit next to the
+        // globally sorted ones): peers by ballots on the varying bits only -- the peer-table
+        // atomics would serialise on the few shared addresses. Padding takes the largest
+        // digit the range can hold, so it still sorts last.
+        const bool narrow = __popc(vmask) <= 3;
+        const std::uint32_t pad_digit =
+            narrow ? ((static_cast<std::uint32_t>(all1 >> (8 * p)) & 0xffu & ~vmask) | vmask) : 255u;
+        for (int i = tid; i < LOCAL_VW * RADIX; i += LOCAL_BLOCK) s_tab[i] = 0;
+        __syncthreads();
+        std::uint32_t dg[ITEMS / 4];
+        std::uint32_t rk[ITEMS / 2];
+#pragma unroll
+        for (int w = 0; w < ITEMS / 4; ++w) dg[w] = 0;
+#pragma unroll
+        for (int w = 0; w < ITEMS / 2; ++w) rk[w] = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const bool ok = base_i + 16 * i < len;
+            const std::uint32_t d = ok ? digit_of(k[i], 8 * p, dsc) : pad_digit;  // padding stays last
+            dg[i / 4] |= d << (8 * (i % 4));
+        }
+        // Padding (slots >= len) takes no part in ranking: it keeps its own slot at the tail,
+        // so it neither counts nor hammers one shared address.
+        if (narrow) {
+            const std::uint32_t half = (lane >> 4) * 16;
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const bool ok = base_i + 16 * i < len;
+                const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+                std::uint32_t m = __ballot_sync(FULL, ok);
+#pragma unroll
+                for (int bb = 0; bb < 8; ++bb) {
+                    if (!((vmask >> bb) & 1u)) continue;  // block-uniform
+                    const std::uint32_t bal = __ballot_sync(FULL, (d >> bb) & 1u);
+                    m &= ((d >> bb) & 1u) ? bal : ~bal;
+                }
+                const std::uint32_t peers = (m >> half) & 0xffffu;
+                __syncwarp();
+                const std::uint32_t base = ld_shared_u32_if(ok, wh + d) >> 16;
+                __syncwarp();
+                const bool lead = ok && (peers & ge16) == bit;
+                st_shared_if(lead, wh + d, (base + __popc(peers)) << 16);
+                rk[i / 2] |= (base + __popc(peers & lt16)) << (16 * (i % 2));
+            }
+        } else {
+            // stable rank inside the half-warp group: word = running count << 16 | peer mask
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const bool ok = base_i + 16 * i < len;
+                const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+                red_or_shared_if(ok, wh + d, bit);
+                __syncwarp();
+                const std::uint32_t w = ld_shared_u32_if(ok, wh + d);
+                __syncwarp();
+                const std::uint32_t peers = w & 0xffffu, base = w >> 16;
+                const bool lead = ok && (peers & ge16) == bit;
+                st_shared_if(lead, wh + d, (base + __popc(peers)) << 16);
+                rk[i / 2] |= (base + __popc(peers & lt16)) << (16 * (i % 2));
+            }
+        }
+        __syncthreads();
+        // digit starts + per-group offsets
+        std::uint32_t total = 0, incl = 0;
+        if (tid < RADIX) {
+#pragma unroll
+            for (int w = 0; w < LOCAL_VW; ++w) {
+                const std::uint32_t cnt = s_tab[w * RADIX + tid] >> 16;
+                s_tab[w * RADIX + tid] = total;
+                total += cnt;
+            }
+            incl = total;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const std::uint32_t y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+        }
+        __syncthreads();
+        if (tid < RADIX) {
+            std::uint32_t wp = 0;
+#pragma unroll
+            for (int w = 0; w < RADIX / 32; ++w)
+                if (w < warp) wp += s_wsum[w];
+            const std::uint32_t dstart = wp + incl - total;
+#pragma unroll
+            for (int w = 0; w < LOCAL_VW; ++w) s_tab[w * RADIX + tid] += dstart;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const std::uint32_t li = base_i + 16 * i;
+            const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
+            if (li < len) s_stage[wh[d] + ((rk[i / 2] >> (16 * (i % 2))) & 0xffffu)] = k[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+            if (base_i + 16 * i < len) k[i] = s_stage[base_i + 16 * i];
+        // (the next pass re-zeroes s_tab only after a barrier; s_stage is rewritten only
+        // after the next pass's ranking barrier, so this reload is complete by then)
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint32_t li = base_i + 16 * i;
+        if (li < len) out[b + li] = k[i];
+    }
+}
+
+// cut j = first index of the bucket (top bits) holding position j*step; cuts[J] = n.
+template <typename T>
+__global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
+                                  std::uint64_t step, std::uint64_t J, std::uint64_t* __restrict__ cuts) {
+    using B = typename key_traits<T>::bits;
+    const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j > J) return;
+    if (j == 0 || j == J) {
+        cuts[j] = j == 0 ? 0 : n;
+        return;
+    }
+    const bool dsc = desc != 0;
+    const std::uint64_t p = j * step;
+    const B t = static_cast<B>(ordered(keys[p], dsc) >> top_shift);
+    std::uint64_t lo = 0, hi = p;
+    while (lo < hi) {
+        const std::uint64_t mid = lo + (hi - lo) / 2;
+        if (static_cast<B>(ordered(keys[mid], dsc) >> top_shift) < t) lo = mid + 1;
+        else hi = mid;
+    }
+    cuts[j] = lo;
+}
+
+// cut b = first index whose top bits are >= b (bucket starts), b in [0, J); cuts[J] = n.
+template <typename T>
+__global__ void bucket_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
+                                   std::uint64_t J, std::uint64_t* __restrict__ cuts) {
+    using B = typename key_traits<T>::bits;
+    const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j > J) return;
+    if (j == J) {
+        cuts[j] = n;
+        return;
+    }
+    const bool dsc = desc != 0;
+    std::uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const std::uint64_t mid = lo + (hi - lo) / 2;
+        if (static_cast<std::uint64_t>(ordered(keys[mid], dsc) >> top_shift) < j) lo = mid + 1;
+        else hi = mid;
+    }
+    cuts[j] = lo;
+}
+
+int hybrid_env() {
+    static const int v = [] {
+        const char* e = std::getenv("AKB_HYBRID");  // "0" disables (plain LSD), "m" forces m top passes
+        return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
+template <typename T, int ITEMS>
+void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc,
+                  std::uint64_t* big) {
+    using LS = local_smem<T, ITEMS>;
+    static bool configured = false;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(local_sort_kernel<T, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(LS::total)));
+        configured = true;
+    }
+    const int tok = ctx_prof_begin(c, KF_LOCAL);
+    local_sort_kernel<T, ITEMS><<<static_cast<unsigned>(J), LOCAL_BLOCK, LS::total, c->stream>>>(G, kout, cuts,
+                                                                                                 desc ? 1 : 0, big);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 1;
+}
+
+// Returns false when the plain LSD should be used instead.
+template <typename T>
+bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
+    constexpr int PASSES = key_traits<T>::nbits / 8;
+    const int env = hybrid_env();
+    if (env == 0 || PASSES != 8) return false;  // 64-bit keys: 32-bit keys keep the 4-pass LSD
+    if (n == 0) return true;
+    // m top digits sorted globally; ranges = single buckets (bucket mode, large buckets)
+    // or runs of small buckets cut every `step` keys (step mode)
+    int m = 0, items = LOCAL_MAX_ITEMS;
+    bool bucket_mode = false;
+    std::uint64_t step = n;
+    if (n > static_cast<std::uint64_t>(LOCAL_TILE)) {
+        double mean = static_cast<double>(n);
+        for (m = 1; m <= 3; ++m) {
+            mean /= 256.0;
+            const double need = mean + 6.0 * std::sqrt(mean) + 64.0;
+            if (need > LOCAL_TILE) continue;
+            if (env > 0 && env != m) continue;
+            const int ib = need <= LOCAL_BLOCK * 8 ? 8 : (need <= LOCAL_BLOCK * 12 ? 12 : 16);
+            if (mean >= 0.55 * LOCAL_BLOCK * ib) {  // one bucket fills most of an ib-item CTA
+                bucket_mode = true;
+                items = ib;
+            } else {
+                step = static_cast<std::uint64_t>(LOCAL_TILE - need);
+                if (step < 256) step = 256;
+            }
+            break;
+        }
+        if (m > 3) return false;
+    }
+    const std::uint64_t J = m == 0 ? 1 : (bucket_mode ? (1ull << (8 * m)) : ceil_div(n, step));
+
+    const T* G = kin;  // buffer holding the bucket-ordered keys
+    if (m > 0) {
+        std::uint64_t* g_hist = static_cast<std::uint64_t*>(c->small);
+        std::uint64_t* g_offs = g_hist + PASSES * RADIX;
+        std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
+        AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
+        const int blocks = c->sm_count * 4;
+        const int tok = ctx_prof_begin(c, KF_HIST);
+        if (m == 1) hist_kernel<T, PASSES, PASSES - 1><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
+        else if (m == 2) hist_kernel<T, PASSES, PASSES - 2><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
+        else hist_kernel<T, PASSES, PASSES - 3><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
+        AKB_CUDA(cudaGetLastError());
+        ctx_prof_end(c, tok);
+        hist_scan_kernel<<<PASSES, RADIX, 0, c->stream>>>(g_hist, g_offs);
+        AKB_CUDA(cudaGetLastError());
+        c->kernel_launches += 2;
+        const T* cur = kin;
+        for (int q = 0; q < m; ++q) {
+            const int p = PASSES - m + q;
+            T* dst = (q % 2 == 0) ? kalt : kout;
+            launch_pass<T, std::uint32_t, SORT_KEYS>(c, cur, dst, nullptr, nullptr, n, 8 * p, desc, p,
+                                                     g_offs + p * RADIX, counters + p, true);
+            cur = dst;
+        }
+        G = cur;
+    }
+    std::uint64_t* cuts = ctx_cuts(c, 2 * J + 3);
+    std::uint64_t* big = cuts + J + 1;
+    AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
+    const int top_shift = key_traits<T>::nbits - 8 * (m > 0 ? m : 1);
+    if (bucket_mode)
+        bucket_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
+            G, n, top_shift, desc ? 1 : 0, J, cuts);
+    else
+        range_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
+            G, n, top_shift, desc ? 1 : 0, step, J, cuts);
+    AKB_CUDA(cudaGetLastError());
+    c->kernel_launches += 1;
+    if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, big);
+    else if (items == 12) launch_local<T, 12>(c, G, kout, cuts, J, desc, big);
+    else launch_local<T, 16>(c, G, kout, cuts, J, desc, big);
+    if (m == 0) return true;  // a single range of <= LOCAL_TILE keys always fits
+    // oversized ranges (skewed keys): plain LSD on each such segment
+    std::uint64_t* h = static_cast<std::uint64_t*>(ctx_pinned(c, sizeof(std::uint64_t)));
+    AKB_CUDA(cudaMemcpyAsync(h, big, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));
+    const std::uint64_t nbig = h[0];
+    if (nbig) {
+        std::vector<std::uint64_t> hc(J + 1), hl(nbig);
+        AKB_CUDA(cudaMemcpy(hc.data(), cuts, (J + 1) * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+        AKB_CUDA(cudaMemcpy(hl.data(), big + 1, nbig * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+        for (std::uint64_t r : hl) {
+            const std::uint64_t b = hc[r], len = hc[r + 1] - hc[r];
+            if (G != kout)
+                AKB_CUDA(cudaMemcpyAsync(kout + b, G + b, len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+            T* scratch = (G == kout) ? kalt + b : const_cast<T*>(G) + b;
+            radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout + b, kout + b, scratch, nullptr, nullptr, nullptr,
+                                                         len, desc, true);
+        }
+    }
+    return true;
+}
+
 }  // namespace
 
 template <typename T, typename V>
@@ -703,7 +1099,8 @@ void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vi
                 std::uint64_t n, bool desc, bool keys_out) {
     switch (mode) {
         case SORT_KEYS:
-            radix_sort_impl<T, V, SORT_KEYS>(c, kin, kout, kalt, nullptr, nullptr, nullptr, n, desc, true);
+            if (!hybrid_sort_keys<T>(c, kin, kout, kalt, n, desc))
+                radix_sort_impl<T, V, SORT_KEYS>(c, kin, kout, kalt, nullptr, nullptr, nullptr, n, desc, true);
             break;
         case SORT_PAIRS:
             radix_sort_impl<T, V, SORT_PAIRS>(c, kin, kout, kalt, vin, vout, valt, n, desc, true);
