@@ -1,0 +1,84 @@
+"""GPU parity of the hybrid 64-bit keys sort (radix_sort.cu: hybrid_sort_keys).
+
+The hybrid picks (m global top-digit passes, bucket/step range mode, 8/12/16-item local
+CTAs) from n, and falls back to the segment LSD for ranges that do not fit on chip. These
+sizes and distributions drive every branch: single-CTA (n <= 6144), m = 1 bucket mode,
+m = 2 step mode, m = 2 bucket mode with 8- and 12-item CTAs, narrow bucket digits, and
+oversized ranges (few distinct top bits, heavy duplicates, clusters). Keys-only integer
+sorts have a unique answer, so numpy's sort is an exact oracle at sizes the C oracle would
+take minutes on; the C oracle is used where it is fast.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [6144, 6145, 50_000, 1 << 20, (1 << 22) + 3, 3 << 23, 1 << 27]
+
+
+def dist(rng, n, kind, dt=np.int64):
+    info = np.iinfo(dt)
+    if kind == "uniform":
+        return rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+    if kind == "low40":  # top 24 bits constant: one giant bucket -> oversized-range fallback
+        return rng.integers(0, 1 << 40, n, dtype=np.int64).astype(dt)
+    if kind == "dups":  # heavy duplicates spread over the key space
+        pool = rng.integers(info.min, info.max, 97, dtype=dt, endpoint=True)
+        return pool[rng.integers(0, 97, n)]
+    if kind == "cluster":  # half the keys in one bucket, half uniform
+        x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        x[: n // 2] = (x[: n // 2] & 0xFFFF) + (0x1234 << 40)
+        rng.shuffle(x)
+        return x
+    if kind == "sorted":
+        return np.sort(rng.integers(info.min, info.max, n, dtype=dt, endpoint=True))
+    if kind == "reversed":
+        return np.sort(rng.integers(info.min, info.max, n, dtype=dt, endpoint=True))[::-1].copy()
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_hybrid_uniform_sizes(ak, ex, dev, n):
+    x = ak.bench_keys(42, 3, n, np.int64)
+    d = torch.from_numpy(x).to(dev)
+    s = torch.empty_like(d)
+    ak.merge_sort(d, s, ex)
+    assert np.array_equal(d.cpu().numpy(), np.sort(x))
+
+
+@pytest.mark.parametrize("kind", ["low40", "dups", "cluster", "sorted", "reversed"])
+@pytest.mark.parametrize("n", [50_000, 1 << 20, 3 << 22])
+def test_hybrid_distributions(ak, ex, dev, kind, n):
+    x = dist(np.random.default_rng(n + len(kind)), n, kind)
+    d = torch.from_numpy(x).to(dev)
+    ak.merge_sort(d, ex=ex)
+    assert np.array_equal(d.cpu().numpy(), np.sort(x))
+
+
+@pytest.mark.parametrize("n", [6145, 1 << 20, 3 << 22])
+def test_hybrid_descending_uint64(ak, ex, dev, n):
+    x = dist(np.random.default_rng(n), n, "uniform", np.uint64)
+    d = torch.from_numpy(x.view(np.int64)).to(dev)
+    ak.merge_sort(d.view(torch.uint64), ex=ex, cmp="greater")
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), np.sort(x)[::-1])
+
+
+def test_hybrid_out_of_place_copy(ak, orc, ex, dev):
+    # merge_sort_copy: input untouched, output sorted (kin != kout path of the hybrid)
+    x = ak.bench_keys(7, 0, 300_001, np.int64)
+    d = torch.from_numpy(x).to(dev)
+    y = ak.merge_sort_copy(d, ex=ex)
+    assert np.array_equal(d.cpu().numpy(), x)
+    assert np.array_equal(y.cpu().numpy(), orc.merge_sort(x))
+
+
+def test_hybrid_f64_keys_bit_exact(ak, orc, ex, dev):
+    # 64-bit float keys go through the hybrid too: -0.0 == +0.0 keeps input order
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1e6, 1e6, 200_000)
+    x[rng.integers(0, x.size, 5000)] = 0.0
+    x[rng.integers(0, x.size, 5000)] = -0.0
+    d = torch.from_numpy(x).to(dev)
+    ak.merge_sort(d, ex=ex)
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), orc.merge_sort(x).view(np.uint64))

@@ -1,6 +1,6 @@
 """Summarise ncu outputs into the tracked profiles/ directory.
 
-    python tools/ncu_summary.py full  <report.ncu-rep> [--keys N]     # --set full capture
+    python tools/ncu_summary.py full  <report.ncu-rep | raw.csv> [--keys N]   # --set full capture
     python tools/ncu_summary.py launches <launches.csv>               # gpu__time_duration list
 
 `full` prints, per profiled launch, the metrics the roofline uses (duration, DRAM
@@ -40,7 +40,10 @@ def _val(v, unit):
 
 
 def full(path, keys=None):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` output saved on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     name_i = hdr.index("Kernel Name")
