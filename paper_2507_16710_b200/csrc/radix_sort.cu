@@ -739,6 +739,7 @@ constexpr int LOCAL_MAX_ITEMS = 16;
 constexpr int LOCAL_TILE = LOCAL_BLOCK * LOCAL_MAX_ITEMS;  // 6144 keys per range at most
 constexpr int LOCAL_VW = LOCAL_BLOCK / 16;                  // half-warp ranking groups
 constexpr int LOCAL_WARPS = LOCAL_BLOCK / 32;
+constexpr std::uint32_t LOCAL_MAX_RUN = 64;  // longest run the insertion fix-up takes on
 
 template <typename T, int ITEMS>
 struct local_smem {
@@ -754,7 +755,7 @@ struct local_smem {
 template <typename T, int ITEMS>
 __global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3 : 2))
     local_sort_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
-                      int desc, std::uint64_t* big) {
+                      int desc, int low, std::uint64_t* big) {
     using L = local_smem<T, ITEMS>;
     using B = typename key_traits<T>::bits;
     constexpr int CAP = LOCAL_BLOCK * ITEMS;
@@ -764,6 +765,7 @@ __global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3
     std::uint32_t* s_tab = reinterpret_cast<std::uint32_t*>(smem + L::tab_off);
     std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
     B* s_red = reinterpret_cast<B*>(smem + L::red_off);
+    std::uint32_t* s_maxrun = s_wsum + 8;
 
     const std::uint64_t b = cuts[blockIdx.x], e = cuts[blockIdx.x + 1];
     if (b >= e) return;
@@ -813,10 +815,10 @@ __global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3
     const std::uint32_t bit = 1u << gl;
     const std::uint32_t lt16 = bit - 1u;
     const std::uint32_t ge16 = 0xffffu & ~lt16;
-#pragma unroll 1
-    for (int p = 0; p < PASSES; ++p) {
+    // one stable local pass over digit p (p varies inside the range): rank the register
+    // keys, stage them in digit order in shared memory, reload them in the new order
+    auto do_pass = [&](int p) {
         const std::uint32_t vmask = static_cast<std::uint32_t>(vary >> (8 * p)) & 0xffu;
-        if (vmask == 0) continue;  // block-uniform
         // Narrow digits (<= 8 distinct values in this range, e.g. the bucket digit next to the
         // globally sorted ones): peers by ballots on the varying bits only -- the peer-table
         // atomics would serialise on the few shared addresses. Padding takes the largest
@@ -918,12 +920,74 @@ __global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3
             if (base_i + 16 * i < len) k[i] = s_stage[base_i + 16 * i];
         // (the next pass re-zeroes s_tab only after a barrier; s_stage is rewritten only
         // after the next pass's ranking barrier, so this reload is complete by then)
-    }
+    };
+
+    // Radix passes only over the digits >= low (the high digits); then keys equal in all
+    // bits >= 8*low form short runs (uniform keys: ~3% of keys, runs of 2-3), which one
+    // thread per run finishes with a stable insertion sort on the full key. If some run is
+    // long (clustered keys) the remaining low digits are radix-passed instead.
+    int passes = 0;
+#pragma unroll 1
+    for (int p = low; p < PASSES; ++p)
+        if ((vary >> (8 * p)) & 0xffu) {
+            do_pass(p);
+            ++passes;
+        }
+    if (passes == 0) {
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const std::uint32_t li = base_i + 16 * i;
-        if (li < len) out[b + li] = k[i];
+        for (int i = 0; i < ITEMS; ++i)
+            if (base_i + 16 * i < len) s_stage[base_i + 16 * i] = k[i];
     }
+    const B lowbits = vary & (8 * low >= key_traits<T>::nbits ? static_cast<B>(~B(0))
+                                                              : static_cast<B>((B(1) << (8 * low)) - 1));
+    if (low > 0 && lowbits != 0) {
+        const B hi_mask = static_cast<B>(~((B(1) << (8 * low)) - 1));
+        if (tid == 0) *s_maxrun = 0;
+        __syncthreads();
+        // phase 1: longest run of equal high bits
+        std::uint32_t mymax = 1;
+        for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) {
+            const B hj = ordered(s_stage[j], dsc) & hi_mask;
+            if (j > 0 && (ordered(s_stage[j - 1], dsc) & hi_mask) == hj) continue;  // not a run start
+            std::uint32_t e2 = j + 1;
+            while (e2 < len && (ordered(s_stage[e2], dsc) & hi_mask) == hj && e2 - j <= LOCAL_MAX_RUN) ++e2;
+            mymax = e2 - j > mymax ? e2 - j : mymax;
+        }
+        if (mymax > 1) atomicMax(s_maxrun, mymax);
+        __syncthreads();
+        if (*s_maxrun <= LOCAL_MAX_RUN) {
+            // phase 2: stable insertion sort of every run on the full key
+            for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) {
+                const B hj = ordered(s_stage[j], dsc) & hi_mask;
+                if (j > 0 && (ordered(s_stage[j - 1], dsc) & hi_mask) == hj) continue;
+                std::uint32_t e2 = j + 1;
+                while (e2 < len && (ordered(s_stage[e2], dsc) & hi_mask) == hj) ++e2;
+                for (std::uint32_t x = j + 1; x < e2; ++x) {
+                    const T v = s_stage[x];
+                    const B ov = ordered(v, dsc);
+                    std::uint32_t y = x;
+                    while (y > j && ordered(s_stage[y - 1], dsc) > ov) {
+                        s_stage[y] = s_stage[y - 1];
+                        --y;
+                    }
+                    s_stage[y] = v;
+                }
+            }
+        } else {
+            // long runs: radix-pass the low digits too, then the high digits again
+            // (every pass is stable, so the result is still the stable sort)
+#pragma unroll 1
+            for (int p = 0; p < low; ++p)
+                if ((vary >> (8 * p)) & 0xffu) do_pass(p);
+#pragma unroll 1
+            for (int p = low; p < PASSES; ++p)
+                if ((vary >> (8 * p)) & 0xffu) do_pass(p);
+        }
+        __syncthreads();
+    } else {
+        __syncthreads();
+    }
+    for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) out[b + j] = s_stage[j];
 }
 
 // cut j = first index of the bucket (top bits) holding position j*step; cuts[J] = n.
@@ -979,7 +1043,7 @@ int hybrid_env() {
 }
 
 template <typename T, int ITEMS>
-void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc,
+void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc, int low,
                   std::uint64_t* big) {
     using LS = local_smem<T, ITEMS>;
     static bool configured = false;
@@ -989,8 +1053,8 @@ void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std
         configured = true;
     }
     const int tok = ctx_prof_begin(c, KF_LOCAL);
-    local_sort_kernel<T, ITEMS><<<static_cast<unsigned>(J), LOCAL_BLOCK, LS::total, c->stream>>>(G, kout, cuts,
-                                                                                                 desc ? 1 : 0, big);
+    local_sort_kernel<T, ITEMS><<<static_cast<unsigned>(J), LOCAL_BLOCK, LS::total, c->stream>>>(
+        G, kout, cuts, desc ? 1 : 0, low, big);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     c->kernel_launches += 1;
@@ -1067,9 +1131,14 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
             G, n, top_shift, desc ? 1 : 0, step, J, cuts);
     AKB_CUDA(cudaGetLastError());
     c->kernel_launches += 1;
-    if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, big);
-    else if (items == 12) launch_local<T, 12>(c, G, kout, cuts, J, desc, big);
-    else launch_local<T, 16>(c, G, kout, cuts, J, desc, big);
+    // local radix passes cover the two digits under the bucket digits; the rest is the
+    // run fix-up (AKB_LOCAL_LOW overrides: 0 = radix-pass every varying digit)
+    int low = PASSES - m - 2;
+    if (low < 0) low = 0;
+    if (const char* e = std::getenv("AKB_LOCAL_LOW")) low = std::atoi(e);
+    if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, low, big);
+    else if (items == 12) launch_local<T, 12>(c, G, kout, cuts, J, desc, low, big);
+    else launch_local<T, 16>(c, G, kout, cuts, J, desc, low, big);
     if (m == 0) return true;  // a single range of <= LOCAL_TILE keys always fits
     // oversized ranges (skewed keys): plain LSD on each such segment
     std::uint64_t* h = static_cast<std::uint64_t*>(ctx_pinned(c, sizeof(std::uint64_t)));
