@@ -31,6 +31,13 @@ def dist(rng, n, kind, dt=np.int64):
         x[: n // 2] = (x[: n // 2] & 0xFFFF) + (0x1234 << 40)
         rng.shuffle(x)
         return x
+    if kind == "midconst":  # bits 16..47 constant: every bucket is one long run of equal high bits
+        x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        return (x & ~np.int64(0xFFFFFFFF0000)) | np.int64(0x5A5A5A5A0000)
+    if kind == "runs40":  # high 32 bits from a pool of n/40 values: runs of ~40 for the insertion fix-up
+        pool = rng.integers(-(1 << 31), 1 << 31, max(1, n // 40), dtype=np.int64)
+        hi = pool[rng.integers(0, pool.size, n)] << 32
+        return hi | rng.integers(0, 1 << 32, n, dtype=np.int64)
     if kind == "sorted":
         return np.sort(rng.integers(info.min, info.max, n, dtype=dt, endpoint=True))
     if kind == "reversed":
@@ -47,7 +54,7 @@ def test_hybrid_uniform_sizes(ak, ex, dev, n):
     assert np.array_equal(d.cpu().numpy(), np.sort(x))
 
 
-@pytest.mark.parametrize("kind", ["low40", "dups", "cluster", "sorted", "reversed"])
+@pytest.mark.parametrize("kind", ["low40", "dups", "cluster", "midconst", "runs40", "sorted", "reversed"])
 @pytest.mark.parametrize("n", [50_000, 1 << 20, 3 << 22])
 def test_hybrid_distributions(ak, ex, dev, kind, n):
     x = dist(np.random.default_rng(n + len(kind)), n, kind)
