@@ -176,28 +176,42 @@ __global__ void __launch_bounds__(RED_BLOCK)
 // Floats accumulate in double (acc_of), so carries over ~2^18 tiles stay exact
 // enough for the 1e-5 contract.
 // ---------------------------------------------------------------------------
-constexpr int SCAN_BLOCK = 256;
-
 template <typename T>
 struct scan_cfg {
-    static constexpr int ITEMS = 16;
-    static constexpr int TILE = SCAN_BLOCK * ITEMS;
+    // 256 threads and 32 KB tiles for every element size (16 x 8 B or 32 x 4 B per thread);
+    // 4 tiles in flight per SM hide the look-back round trips.
+    static constexpr int BLOCK = 256;
+    static constexpr int ITEMS = 32 / sizeof(T) * 4;
+    static constexpr int TILE = BLOCK * ITEMS;
     static constexpr int PADDED = TILE + TILE / ITEMS;  // one pad slot per thread run
     static constexpr int VEC = 16 / sizeof(T);
 };
 
-__device__ __forceinline__ int scan_slot(int e) { return e + (e >> 4); }
+// element e of the tile lives at e + e / ITEMS: each thread's run of ITEMS contiguous
+// elements starts on a different bank (conflict-free blocked reads and writes)
+template <int ITEMS>
+__device__ __forceinline__ int scan_slot(int e) { return e + e / ITEMS; }
+
+// In-thread accumulation type: floats scan their 32-element run in float (error ~1e-7 of
+// the run) and carry everything beyond the run in double (acc_of).
+template <typename T>
+struct local_acc_of {
+    using type = T;
+};
 
 template <typename T, int OP, bool VECIO>
-__global__ void __launch_bounds__(SCAN_BLOCK, 4)
+__global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 4)
     scan_kernel(const T* x, T* out, std::uint64_t n, T init, int inclusive, std::uint32_t* flags,
                 std::uint64_t* vals, std::uint32_t tag, std::uint32_t* tile_counter) {
     using A = typename acc_of<T>::type;
     using F = opf<A, OP>;
+    using LA = typename local_acc_of<T>::type;
+    using FL = opf<LA, OP>;
     using Cfg = scan_cfg<T>;
     constexpr int ITEMS = Cfg::ITEMS;
     constexpr int TILE = Cfg::TILE;
     constexpr int VEC = Cfg::VEC;
+    constexpr int SCAN_BLOCK = Cfg::BLOCK;
     constexpr int WARPS = SCAN_BLOCK / 32;
     __shared__ __align__(16) T s_tile[Cfg::PADDED];
     __shared__ A s_warp[WARPS];
@@ -222,28 +236,28 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4)
             const T* e = reinterpret_cast<const T*>(&q[j]);
             const int e0 = (j * SCAN_BLOCK + tid) * VEC;
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) s_tile[scan_slot(e0 + k)] = e[k];
+            for (int k = 0; k < VEC; ++k) s_tile[scan_slot<ITEMS>(e0 + k)] = e[k];
         }
     } else {
 #pragma unroll 4
         for (int e = tid; e < TILE; e += SCAN_BLOCK)
-            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot(e)] = x[base + e];
+            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot<ITEMS>(e)] = x[base + e];
     }
     __syncthreads();
 
     // ---- thread-serial scan of 16 contiguous elements ----
     const int my0 = tid * ITEMS;
-    A v[ITEMS];
-    A run = F::identity();
+    LA v[ITEMS];
+    LA run = FL::identity();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const bool ok = full || static_cast<std::uint64_t>(my0 + i) < rem;
-        const A xi = ok ? static_cast<A>(s_tile[scan_slot(my0 + i)]) : F::identity();
-        run = F::apply(run, xi);
+        const LA xi = ok ? static_cast<LA>(s_tile[scan_slot<ITEMS>(my0 + i)]) : FL::identity();
+        run = FL::apply(run, xi);
         v[i] = run;  // thread-local inclusive prefix
     }
     // warp scan of thread totals
-    A winc = run;
+    A winc = static_cast<A>(run);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const A y = shfl_up_any(winc, o);
@@ -324,11 +338,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4)
     const A pre = F::apply(F::apply(F::apply(static_cast<A>(init), s_excl), wexcl), texcl);
     if (inclusive) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) s_tile[scan_slot(my0 + i)] = static_cast<T>(F::apply(pre, v[i]));
+        for (int i = 0; i < ITEMS; ++i) s_tile[scan_slot<ITEMS>(my0 + i)] = static_cast<T>(F::apply(pre, static_cast<A>(v[i])));
     } else {
-        s_tile[scan_slot(my0)] = static_cast<T>(pre);
+        s_tile[scan_slot<ITEMS>(my0)] = static_cast<T>(pre);
 #pragma unroll
-        for (int i = 1; i < ITEMS; ++i) s_tile[scan_slot(my0 + i)] = static_cast<T>(F::apply(pre, v[i - 1]));
+        for (int i = 1; i < ITEMS; ++i) s_tile[scan_slot<ITEMS>(my0 + i)] = static_cast<T>(F::apply(pre, static_cast<A>(v[i - 1])));
     }
     __syncthreads();
 
@@ -341,13 +355,13 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4)
             T* e = reinterpret_cast<T*>(&q);
             const int e0 = (j * SCAN_BLOCK + tid) * VEC;
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) e[k] = s_tile[scan_slot(e0 + k)];
+            for (int k = 0; k < VEC; ++k) e[k] = s_tile[scan_slot<ITEMS>(e0 + k)];
             dst[j * SCAN_BLOCK + tid] = q;
         }
     } else {
 #pragma unroll 4
         for (int e = tid; e < TILE; e += SCAN_BLOCK)
-            if (static_cast<std::uint64_t>(e) < rem) out[base + e] = s_tile[scan_slot(e)];
+            if (static_cast<std::uint64_t>(e) < rem) out[base + e] = s_tile[scan_slot<ITEMS>(e)];
     }
 }
 
@@ -397,7 +411,7 @@ void scan(ak_ctx* c, const T* x, T* out, std::uint64_t n, int op, int inclusive,
     const int tok = ctx_prof_begin(c, KF_SCAN);
     const bool vecio = ((reinterpret_cast<std::uintptr_t>(x) | reinterpret_cast<std::uintptr_t>(out)) & 15) == 0;
 #define AKB_SCAN(OPV, V)                                                                       \
-    scan_kernel<T, OPV, V><<<static_cast<unsigned>(tiles), SCAN_BLOCK, 0, c->stream>>>(         \
+    scan_kernel<T, OPV, V><<<static_cast<unsigned>(tiles), scan_cfg<T>::BLOCK, 0, c->stream>>>(         \
         x, out, n, init, inclusive, c->scan_flags, c->scan_vals, tag, counter)
     if (vecio) {
         if (op == OP_SUM) AKB_SCAN(OP_SUM, true);
