@@ -130,6 +130,10 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int key_bytes);
     /* for integers; floats accumulate in double) */                                            \
     int ak_accumulate_##S(ak_ctx* ctx, const T* x, uint64_t n, T* out, uint64_t out_n, int op,   \
                           int inclusive, T init, uint64_t chunk_size);                          \
+    /* stable P-way merge of sorted device runs, ties to the lower run (the second local sort  */ \
+    /* of sihsort.hpp:555 as a merge); 1 <= P <= 4096; scratch >= sum(lens) elements */          \
+    int ak_merge_runs_##S(ak_ctx* ctx, int P, const T* const* runs, const uint64_t* lens, T* dst,  \
+                          T* scratch, int desc);                                                \
     /* searchsorted (search.hpp:36-50): side 0 first, 1 last; out: device uint64[m] */          \
     int ak_searchsorted_##S(ak_ctx* ctx, const T* hay, uint64_t n, const T* needles,            \
                             uint64_t m, int side_last, int desc, int validate, uint64_t* out);   \

@@ -496,6 +496,31 @@ def searchsorted(haystack: torch.Tensor, needles: torch.Tensor, side: str = "fir
     return out
 
 
+def merge_runs(runs: list, out: torch.Tensor | None = None, ex: ExecBackend | None = None, cmp=None,
+               scratch: torch.Tensor | None = None) -> torch.Tensor:
+    """Stable P-way merge of sorted device runs (1 <= P <= 4096); equal keys keep run order,
+    i.e. the result is the stable sort of the runs' concatenation (sihsort.hpp:555)."""
+    if not runs:
+        raise InvalidArgument("merge_runs: no runs")
+    for r in runs:
+        _dev(r, "merge_runs")
+        if r.dtype != runs[0].dtype:
+            raise InvalidArgument("merge_runs: runs must share a dtype")
+    e = _ex(ex, runs[0])
+    total = sum(r.numel() for r in runs)
+    if out is None:
+        out = torch.empty(total, dtype=runs[0].dtype, device=runs[0].device)
+    if scratch is None:
+        scratch = torch.empty(max(total, 1), dtype=runs[0].dtype, device=runs[0].device)
+    P = len(runs)
+    ptrs = (C.c_void_p * P)(*[_ptr(r) for r in runs])
+    lens = (C.c_uint64 * P)(*[r.numel() for r in runs])
+    fn = _fn(f"ak_merge_runs_{_suffix(runs[0])}", [_P, C.c_int, _P, _P, _P, _P, C.c_int])
+    _check(fn(e.handle, P, C.cast(ptrs, C.c_void_p), C.cast(lens, C.c_void_p), _ptr(out), _ptr(scratch),
+              _desc(cmp)))
+    return out
+
+
 # ----------------------------------------------------------------------------- sihsort
 
 class SihConfig(C.Structure):

@@ -215,6 +215,21 @@ void scan_impl(ak_ctx* c, const T* x, std::uint64_t n, T* out, std::uint64_t out
 }
 
 template <typename T>
+void merge_runs_impl(ak_ctx* c, int P, const T* const* runs, const uint64_t* lens, T* dst, T* scratch, int desc) {
+    ctx_lock g(c);
+    need(P >= 1 && P <= akb::MW_MAXP, "merge_runs: 1 <= P <= 4096 runs");
+    need(runs && lens, "merge_runs: null runs");
+    std::uint64_t total = 0;
+    for (int r = 0; r < P; ++r) {
+        need(lens[r] == 0 || runs[r], "merge_runs: null run");
+        total += lens[r];
+    }
+    need(total == 0 || (dst && scratch), "merge_runs: null output or scratch");
+    akb::merge_runs<T>(c, P, runs, lens, dst, scratch, desc != 0);
+    akb::ctx_finish(c);
+}
+
+template <typename T>
 void search_impl(ak_ctx* c, const T* hay, std::uint64_t n, const T* needles, std::uint64_t m, int side_last,
                  int desc, int validate, std::uint64_t* out) {
     ctx_lock g(c);
@@ -504,6 +519,10 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int kb) {
                           T init, uint64_t chunk) {                                                      \
         return guard([&] { scan_impl<T>(c, x, n, o, on, op, inc, init, chunk); });                       \
     }                                                                                                    \
+    int ak_merge_runs_##S(ak_ctx* c, int P, const T* const* runs, const uint64_t* lens, T* dst, T* scratch,  \
+                          int desc) {                                                                  \
+        return guard([&] { merge_runs_impl<T>(c, P, runs, lens, dst, scratch, desc); });               \
+    }                                                                                                   \
     int ak_searchsorted_##S(ak_ctx* c, const T* h, uint64_t n, const T* nd, uint64_t m, int last,       \
                             int desc, int validate, uint64_t* o) {                                      \
         return guard([&] { search_impl<T>(c, h, n, nd, m, last, desc, validate, o); });                  \

@@ -13,6 +13,7 @@
 //   5. windowed decoupled look-back (4 predecessors in flight per digit) ->
 //      INC publish and global digit bases;
 //   6. scatter contiguous per-digit runs.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1016,7 +1017,7 @@ __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, i
 // cut b = first index whose top bits are >= b (bucket starts), b in [0, J); cuts[J] = n.
 template <typename T>
 __global__ void bucket_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
-                                   std::uint64_t J, std::uint64_t* __restrict__ cuts) {
+                                   std::uint64_t J, std::uint64_t base_id, std::uint64_t* __restrict__ cuts) {
     using B = typename key_traits<T>::bits;
     const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j > J) return;
@@ -1028,7 +1029,7 @@ __global__ void bucket_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, 
     std::uint64_t lo = 0, hi = n;
     while (lo < hi) {
         const std::uint64_t mid = lo + (hi - lo) / 2;
-        if (static_cast<std::uint64_t>(ordered(keys[mid], dsc) >> top_shift) < j) lo = mid + 1;
+        if (static_cast<std::uint64_t>(ordered(keys[mid], dsc) >> top_shift) < base_id + j) lo = mid + 1;
         else hi = mid;
     }
     cuts[j] = lo;
@@ -1061,26 +1062,91 @@ void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std
 }
 
 // Returns false when the plain LSD should be used instead.
+//
+// The plan is read off the data: one histogram pass over the top three digits (plus all
+// eight when those are constant) gives, per digit, its largest bin. Constant leading digits
+// are skipped; the bucket size after m global passes over the next digits is estimated as
+// n * prod(max bin / n) (exact for m = 1, independence otherwise), and the smallest m whose
+// buckets fit a CTA is taken. Skewed inputs thus get more global digits instead of
+// oversized ranges; a mis-estimate only costs the (bounded) segment fallback.
 template <typename T>
 bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
     constexpr int PASSES = key_traits<T>::nbits / 8;
     const int env = hybrid_env();
     if (env == 0 || PASSES != 8) return false;  // 64-bit keys: 32-bit keys keep the 4-pass LSD
     if (n == 0) return true;
-    // m top digits sorted globally; ranges = single buckets (bucket mode, large buckets)
-    // or runs of small buckets cut every `step` keys (step mode)
-    int m = 0, items = LOCAL_MAX_ITEMS;
+    std::uint64_t* g_hist = static_cast<std::uint64_t*>(c->small);
+    std::uint64_t* g_offs = g_hist + PASSES * RADIX;
+    std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
+    int m = 0, top = PASSES, items = LOCAL_MAX_ITEMS;
     bool bucket_mode = false;
-    std::uint64_t step = n;
+    std::uint64_t step = n, J = 1, base_id = 0;
+    const T* G = kin;  // buffer holding the bucket-ordered keys
     if (n > static_cast<std::uint64_t>(LOCAL_TILE)) {
-        double mean = static_cast<double>(n);
-        for (m = 1; m <= 3; ++m) {
-            mean /= 256.0;
-            const double need = mean + 6.0 * std::sqrt(mean) + 64.0;
+        const int blocks = c->sm_count * 4;
+        AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
+        int first = PASSES - 3;
+        auto run_hist = [&](int f) {
+            const int tok = ctx_prof_begin(c, KF_HIST);
+            if (f == PASSES - 3) hist_kernel<T, PASSES, PASSES - 3><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
+            else hist_kernel<T, PASSES, 0><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
+            AKB_CUDA(cudaGetLastError());
+            ctx_prof_end(c, tok);
+            c->kernel_launches += 1;
+        };
+        run_hist(first);
+        std::vector<std::uint64_t> h(PASSES * RADIX);
+        auto fetch = [&] {
+            std::uint64_t* hp = static_cast<std::uint64_t*>(ctx_pinned(c, PASSES * RADIX * sizeof(std::uint64_t)));
+            AKB_CUDA(cudaMemcpyAsync(hp, g_hist, PASSES * RADIX * sizeof(std::uint64_t), cudaMemcpyDeviceToHost,
+                                     c->stream));
+            AKB_CUDA(cudaStreamSynchronize(c->stream));
+            std::copy(hp, hp + PASSES * RADIX, h.begin());
+        };
+        fetch();
+        auto maxbin = [&](int d, int* which) {
+            std::uint64_t mx = 0;
+            for (int i = 0; i < RADIX; ++i)
+                if (h[d * RADIX + i] > mx) {
+                    mx = h[d * RADIX + i];
+                    if (which) *which = i;
+                }
+            return mx;
+        };
+        // skip constant leading digits (their value becomes the bucket-id prefix)
+        std::uint64_t prefix = 0;
+        for (;;) {
+            if (top == first) {
+                if (first == 0) break;
+                AKB_CUDA(cudaMemsetAsync(g_hist, 0, PASSES * RADIX * 8, c->stream));
+                first = 0;
+                run_hist(0);
+                fetch();
+            }
+            int v = 0;
+            if (maxbin(top - 1, &v) != n) break;
+            prefix = (prefix << 8) | static_cast<std::uint64_t>(v);
+            --top;
+            if (top == 0) break;
+        }
+        if (top == 0) {  // every key equal
+            if (kin != kout) AKB_CUDA(cudaMemcpyAsync(kout, kin, n * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+            return true;
+        }
+        double est = static_cast<double>(n);
+        for (m = 1; m <= 3 && m <= top; ++m) {
+            if (top - m < first) {  // need the histogram of a lower digit
+                AKB_CUDA(cudaMemsetAsync(g_hist, 0, PASSES * RADIX * 8, c->stream));
+                first = 0;
+                run_hist(0);
+                fetch();
+            }
+            est *= static_cast<double>(maxbin(top - m, nullptr)) / static_cast<double>(n);
+            const double need = est + 6.0 * std::sqrt(est) + 64.0;
             if (need > LOCAL_TILE) continue;
             if (env > 0 && env != m) continue;
             const int ib = need <= LOCAL_BLOCK * 8 ? 8 : (need <= LOCAL_BLOCK * 12 ? 12 : 16);
-            if (mean >= 0.55 * LOCAL_BLOCK * ib) {  // one bucket fills most of an ib-item CTA
+            if (est >= 0.55 * LOCAL_BLOCK * ib) {  // one bucket fills most of an ib-item CTA
                 bucket_mode = true;
                 items = ib;
             } else {
@@ -1089,29 +1155,15 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
             }
             break;
         }
-        if (m > 3) return false;
-    }
-    const std::uint64_t J = m == 0 ? 1 : (bucket_mode ? (1ull << (8 * m)) : ceil_div(n, step));
-
-    const T* G = kin;  // buffer holding the bucket-ordered keys
-    if (m > 0) {
-        std::uint64_t* g_hist = static_cast<std::uint64_t*>(c->small);
-        std::uint64_t* g_offs = g_hist + PASSES * RADIX;
-        std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
-        AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
-        const int blocks = c->sm_count * 4;
-        const int tok = ctx_prof_begin(c, KF_HIST);
-        if (m == 1) hist_kernel<T, PASSES, PASSES - 1><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
-        else if (m == 2) hist_kernel<T, PASSES, PASSES - 2><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
-        else hist_kernel<T, PASSES, PASSES - 3><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
-        AKB_CUDA(cudaGetLastError());
-        ctx_prof_end(c, tok);
+        if (m > 3 || m > top) return false;
+        J = bucket_mode ? (1ull << (8 * m)) : ceil_div(n, step);
+        base_id = prefix << (8 * m);
         hist_scan_kernel<<<PASSES, RADIX, 0, c->stream>>>(g_hist, g_offs);
         AKB_CUDA(cudaGetLastError());
-        c->kernel_launches += 2;
+        c->kernel_launches += 1;
         const T* cur = kin;
         for (int q = 0; q < m; ++q) {
-            const int p = PASSES - m + q;
+            const int p = top - m + q;
             T* dst = (q % 2 == 0) ? kalt : kout;
             launch_pass<T, std::uint32_t, SORT_KEYS>(c, cur, dst, nullptr, nullptr, n, 8 * p, desc, p,
                                                      g_offs + p * RADIX, counters + p, true);
@@ -1122,10 +1174,10 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
     std::uint64_t* cuts = ctx_cuts(c, 2 * J + 3);
     std::uint64_t* big = cuts + J + 1;
     AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
-    const int top_shift = key_traits<T>::nbits - 8 * (m > 0 ? m : 1);
+    const int top_shift = 8 * (top - (m > 0 ? m : 1));
     if (bucket_mode)
         bucket_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
-            G, n, top_shift, desc ? 1 : 0, J, cuts);
+            G, n, top_shift, desc ? 1 : 0, J, base_id, cuts);
     else
         range_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
             G, n, top_shift, desc ? 1 : 0, step, J, cuts);
@@ -1133,29 +1185,38 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
     c->kernel_launches += 1;
     // local radix passes cover the two digits under the bucket digits; the rest is the
     // run fix-up (AKB_LOCAL_LOW overrides: 0 = radix-pass every varying digit)
-    int low = PASSES - m - 2;
+    int low = top - m - 2;
     if (low < 0) low = 0;
     if (const char* e = std::getenv("AKB_LOCAL_LOW")) low = std::atoi(e);
     if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, low, big);
     else if (items == 12) launch_local<T, 12>(c, G, kout, cuts, J, desc, low, big);
     else launch_local<T, 16>(c, G, kout, cuts, J, desc, low, big);
     if (m == 0) return true;  // a single range of <= LOCAL_TILE keys always fits
-    // oversized ranges (skewed keys): plain LSD on each such segment
-    std::uint64_t* h = static_cast<std::uint64_t*>(ctx_pinned(c, sizeof(std::uint64_t)));
-    AKB_CUDA(cudaMemcpyAsync(h, big, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    // oversized ranges (skewed keys): plain LSD on each such segment, or on the whole
+    // array when there are many (every range is a stable permutation of its keys, equal
+    // keys never straddle ranges, so a stable sort of the partial result is the answer)
+    std::uint64_t* hb = static_cast<std::uint64_t*>(ctx_pinned(c, sizeof(std::uint64_t)));
+    AKB_CUDA(cudaMemcpyAsync(hb, big, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
     AKB_CUDA(cudaStreamSynchronize(c->stream));
-    const std::uint64_t nbig = h[0];
+    const std::uint64_t nbig = hb[0];
     if (nbig) {
         std::vector<std::uint64_t> hc(J + 1), hl(nbig);
         AKB_CUDA(cudaMemcpy(hc.data(), cuts, (J + 1) * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
         AKB_CUDA(cudaMemcpy(hl.data(), big + 1, nbig * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+        const bool whole = nbig > 32;
         for (std::uint64_t r : hl) {
             const std::uint64_t b = hc[r], len = hc[r + 1] - hc[r];
             if (G != kout)
                 AKB_CUDA(cudaMemcpyAsync(kout + b, G + b, len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+            if (whole) continue;
             T* scratch = (G == kout) ? kalt + b : const_cast<T*>(G) + b;
             radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout + b, kout + b, scratch, nullptr, nullptr, nullptr,
                                                          len, desc, true);
+        }
+        if (whole) {
+            T* scratch = (G == kout) ? kalt : const_cast<T*>(G);
+            radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout, kout, scratch, nullptr, nullptr, nullptr, n, desc,
+                                                         true);
         }
     }
     return true;

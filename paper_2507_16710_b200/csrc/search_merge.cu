@@ -1,6 +1,8 @@
 // search_merge.cu -- searchsorted, sample gather, merge-path 2-way merge, is_sorted.
 #include "search_merge.cuh"
 
+#include <vector>
+
 namespace akb {
 
 namespace {
@@ -66,7 +68,7 @@ __device__ __forceinline__ std::uint64_t co_rank_dev(std::uint64_t k, const T* a
 constexpr int MERGE_BLOCK = 256;
 template <typename T>
 struct merge_cfg {
-    static constexpr int ITEMS = sizeof(T) == 8 ? 12 : 16;
+    static constexpr int ITEMS = sizeof(T) == 8 ? 13 : 17;  // odd: no bank-aligned thread windows
     static constexpr int TILE = MERGE_BLOCK * ITEMS;
 };
 
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(MERGE_BLOCK)
     for (int i = threadIdx.x; i < total; i += MERGE_BLOCK) dst[d0 + i] = s[i];
 }
 
+
 template <typename T>
 __global__ void unsorted_kernel(const T* __restrict__ x, std::uint64_t n, int desc, unsigned* flag) {
     const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
@@ -183,6 +186,52 @@ void merge2(ak_ctx* c, const T* a, std::uint64_t na, const T* b, std::uint64_t n
     c->kernel_launches += 2;
 }
 
+
+// K8: stable P-way merge as a tree of merge-path 2-way merges over HBM, ceil(log2 P)
+// levels ping-ponging between dst and scratch (the last level lands in dst). Measured on
+// B200 (r01): a 2-way level runs at ~3.3 TB/s of key traffic, and a one-pass variant that
+// merged the P pieces of value-cut tiles in shared memory was slower (its on-chip levels are
+// latency-bound, ~0.7 ms per level at 2^27 keys), so the tree stays.
+template <typename T>
+void merge_runs(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* lens, T* dst, T* scratch, bool desc) {
+    if (P < 1) throw invalid_argument("merge_runs: P >= 1 runs");
+    struct run {
+        const T* p;
+        std::uint64_t len, off;
+    };
+    std::vector<run> live;
+    std::uint64_t off = 0;
+    for (int r = 0; r < P; ++r) {
+        if (lens[r]) live.push_back({runs[r], lens[r], off});
+        off += lens[r];
+    }
+    if (live.empty()) return;
+    if (live.size() == 1) {
+        if (live[0].p != dst)
+            AKB_CUDA(cudaMemcpyAsync(dst, live[0].p, live[0].len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    int levels = 0;
+    for (std::size_t m = 1; m < live.size(); m <<= 1) ++levels;
+    for (int l = 1; l <= levels; ++l) {
+        T* out = ((levels - l) % 2 == 0) ? dst : scratch;
+        std::vector<run> next;
+        for (std::size_t i = 0; i < live.size(); i += 2) {
+            if (i + 1 == live.size()) {  // odd run out: moved into this level's buffer
+                const run& a = live[i];
+                AKB_CUDA(cudaMemcpyAsync(out + a.off, a.p, a.len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+                next.push_back({out + a.off, a.len, a.off});
+                continue;
+            }
+            const run& a = live[i];
+            const run& b = live[i + 1];
+            merge2<T>(c, a.p, a.len, b.p, b.len, out + a.off, desc);
+            next.push_back({out + a.off, a.len + b.len, a.off});
+        }
+        live.swap(next);
+    }
+}
+
 template <typename T>
 bool is_sorted(ak_ctx* c, const T* x, std::uint64_t n, bool desc) {
     if (n < 2) return true;
@@ -202,7 +251,8 @@ bool is_sorted(ak_ctx* c, const T* x, std::uint64_t n, bool desc) {
                                   int, std::uint64_t*);                                           \
     template std::uint64_t gather_samples<T>(ak_ctx*, const T*, std::uint64_t, std::uint64_t, T*);  \
     template void merge2<T>(ak_ctx*, const T*, std::uint64_t, const T*, std::uint64_t, T*, bool);   \
-    template bool is_sorted<T>(ak_ctx*, const T*, std::uint64_t, bool);
+    template bool is_sorted<T>(ak_ctx*, const T*, std::uint64_t, bool);                            \
+    template void merge_runs<T>(ak_ctx*, int, const T* const*, const std::uint64_t*, T*, T*, bool);
 
 AKB_INST(std::int32_t)
 AKB_INST(std::uint32_t)

@@ -24,6 +24,12 @@ template <typename T>
 void merge2(ak_ctx* c, const T* a, std::uint64_t na, const T* b, std::uint64_t nb, T* dst,
             bool desc);
 
+// Stable P-way merge of sorted runs (run order breaks ties: the stable sort of their
+// concatenation); scratch: >= total elements of device memory.
+constexpr int MW_MAXP = 4096;  // runs per merge_runs call (C ABI bound)
+template <typename T>
+void merge_runs(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* lens, T* dst, T* scratch, bool desc);
+
 // Is the device array nondecreasing under the comparator? (search.hpp:40-43 validate)
 template <typename T>
 bool is_sorted(ak_ctx* c, const T* x, std::uint64_t n, bool desc);

@@ -1,4 +1,5 @@
 // sihsort.cu -- device policy of the SIHSort protocol, NCCL and loopback transports.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -249,7 +250,7 @@ struct device_local {
     }
 
     // P-way merge of the runs in source-rank order (replaces local sort #2,
-    // sihsort.hpp:555): pairwise merge-path tree, last level lands in d_out.
+    // sihsort.hpp:555): merge_runs (K8), last level lands in d_out.
     std::uint64_t merge_runs(const std::vector<std::uint64_t>& bounds,
                              const std::vector<std::uint64_t>& recv_counts) {
         std::uint64_t total = 0;
@@ -276,35 +277,17 @@ struct device_local {
                                      c->stream));
             return total;
         }
-        int levels = 0;
-        for (std::size_t m = 1; m < live.size(); m <<= 1) ++levels;
-        // base offset of live run i in the output = sum of previous live lengths
-        off = 0;
-        for (auto& rr : live) {
-            rr.off = off;
-            off += rr.len;
-        }
-        for (int l = 1; l <= levels; ++l) {
-            T* dst = ((levels - l) % 2 == 0) ? d_out : X;
-            std::vector<run> next;
-            for (std::size_t i = 0; i < live.size(); i += 2) {
-                if (i + 1 == live.size()) {
-                    // odd run out: move it into this level's buffer so that every source of
-                    // the next level lives in the buffer the next level does not write
-                    const run& a = live[i];
-                    AKB_CUDA(cudaMemcpyAsync(dst + a.off, a.p, a.len * sizeof(T), cudaMemcpyDeviceToDevice,
-                                             c->stream));
-                    next.push_back({dst + a.off, a.len, a.off});
-                    continue;
-                }
-                const run& a = live[i];
-                const run& b = live[i + 1];
-                merge2<T>(c, a.p, a.len, b.p, b.len, dst + a.off, false);
-                next.push_back({dst + a.off, a.len + b.len, a.off});
+        {
+            // P-way merge tree (K8, search_merge.cu); X is free scratch at this point
+            std::vector<const T*> ptrs;
+            std::vector<std::uint64_t> lens;
+            for (auto& rr : live) {
+                ptrs.push_back(rr.p);
+                lens.push_back(rr.len);
             }
-            live.swap(next);
+            akb::merge_runs<T>(c, static_cast<int>(live.size()), ptrs.data(), lens.data(), d_out, X, false);
+            return total;
         }
-        return total;
     }
 };
 
