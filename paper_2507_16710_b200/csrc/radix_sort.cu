@@ -945,38 +945,36 @@ __global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3
         const B hi_mask = static_cast<B>(~((B(1) << (8 * low)) - 1));
         if (tid == 0) *s_maxrun = 0;
         __syncthreads();
-        // phase 1: longest run of equal high bits
-        std::uint32_t mymax = 1;
+        // One scan: a thread owning a run start (first key of a run of equal high bits)
+        // finds the run's end and insertion-sorts it on the full key (stable); runs longer
+        // than LOCAL_MAX_RUN are only flagged. Other threads' sorts permute keys inside their
+        // own runs only, so the high bits read across run borders never change.
         for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) {
             const B hj = ordered(s_stage[j], dsc) & hi_mask;
             if (j > 0 && (ordered(s_stage[j - 1], dsc) & hi_mask) == hj) continue;  // not a run start
             std::uint32_t e2 = j + 1;
-            while (e2 < len && (ordered(s_stage[e2], dsc) & hi_mask) == hj && e2 - j <= LOCAL_MAX_RUN) ++e2;
-            mymax = e2 - j > mymax ? e2 - j : mymax;
-        }
-        if (mymax > 1) atomicMax(s_maxrun, mymax);
-        __syncthreads();
-        if (*s_maxrun <= LOCAL_MAX_RUN) {
-            // phase 2: stable insertion sort of every run on the full key
-            for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) {
-                const B hj = ordered(s_stage[j], dsc) & hi_mask;
-                if (j > 0 && (ordered(s_stage[j - 1], dsc) & hi_mask) == hj) continue;
-                std::uint32_t e2 = j + 1;
-                while (e2 < len && (ordered(s_stage[e2], dsc) & hi_mask) == hj) ++e2;
-                for (std::uint32_t x = j + 1; x < e2; ++x) {
-                    const T v = s_stage[x];
-                    const B ov = ordered(v, dsc);
-                    std::uint32_t y = x;
-                    while (y > j && ordered(s_stage[y - 1], dsc) > ov) {
-                        s_stage[y] = s_stage[y - 1];
-                        --y;
-                    }
-                    s_stage[y] = v;
-                }
+            while (e2 < len && e2 - j <= LOCAL_MAX_RUN && (ordered(s_stage[e2], dsc) & hi_mask) == hj) ++e2;
+            if (e2 - j < 2) continue;
+            if (e2 - j > LOCAL_MAX_RUN) {
+                atomicMax(s_maxrun, e2 - j);
+                continue;
             }
-        } else {
+            for (std::uint32_t x = j + 1; x < e2; ++x) {
+                const T v = s_stage[x];
+                const B ov = ordered(v, dsc);
+                std::uint32_t y = x;
+                while (y > j && ordered(s_stage[y - 1], dsc) > ov) {
+                    s_stage[y] = s_stage[y - 1];
+                    --y;
+                }
+                s_stage[y] = v;
+            }
+        }
+        __syncthreads();
+        if (*s_maxrun > LOCAL_MAX_RUN) {
             // long runs: radix-pass the low digits too, then the high digits again
-            // (every pass is stable, so the result is still the stable sort)
+            // (every pass is stable and the registers still hold the pre-fix-up order,
+            // so the result is the stable sort)
 #pragma unroll 1
             for (int p = 0; p < low; ++p)
                 if ((vary >> (8 * p)) & 0xffu) do_pass(p);
