@@ -94,23 +94,24 @@ std::pair<std::vector<T>, sih_stats> sihsort(std::vector<T> local_data, Comm& co
     detail::require_key<T>();
     const ak_sih_config c = detail::to_c(cfg);
     ak_sih_stats st{};
-    std::uint64_t cap = local_data.size() + local_data.size() / 4 + 4096;
-    std::vector<T> out;
+    const std::uint64_t n = local_data.size();
+    // keys go to HBM once; the output is sized on the device and copied back at its exact length
+    detail::device_buffer<T> din(ex.ctx(), n);
+    din.upload(local_data.data(), n);
+    std::uint64_t cap = n + n / 4 + 4096;
+    std::uint64_t count = 0;
     for (;;) {
-        out.resize(cap);
-        std::uint64_t count = 0;
-        const int rc = detail::c_sihsort_host(ex.ctx(), comm.handle(), local_data.data(), local_data.size(),
-                                              out.data(), cap, &count, &c, &st);
+        detail::device_buffer<T> dout(ex.ctx(), cap);
+        const int rc = detail::c_sihsort(ex.ctx(), comm.handle(), din.p, n, dout.p, cap, &count, &c, &st);
         if (rc == AK_ECAPACITY) {  // raised on every rank together: all retry with room
-            cap = count > cap ? count : cap;
-            cap += cap / 8 + 4096;
+            cap = (count > cap ? count : cap) + cap / 8 + 4096;
             continue;
         }
         detail::check(rc, count);
-        out.resize(count);
-        break;
+        std::vector<T> out(count);
+        dout.download(out.data(), count);
+        return {std::move(out), detail::from_c(st)};
     }
-    return {std::move(out), detail::from_c(st)};
 }
 
 /// Sorter-slot overload (sihsort.hpp:508): ak::cuda_sorter selects the device pipeline.

@@ -17,7 +17,9 @@
 #include <span>
 #include <vector>
 
+#include "ak/csv.hpp"
 #include "ak/exec.hpp"
+#include "ak/fixture.hpp"
 #include "ak/reduce.hpp"
 #include "ak/scan.hpp"
 #include "ak/search.hpp"
@@ -263,4 +265,44 @@ REF_API std::uint64_t ref_sortperm_bytes(std::uint64_t n, int key_bytes, int ind
                       : ak::sortperm_buffers<float, std::int32_t>::required_bytes(n);
     }
     return 0;
+}
+
+// ---- SIHS fixtures and benchmark CSV (reference src/fixture.cpp, src/csv.cpp) ----
+#define REF_FIXTURE(SUF, T)                                                                           \
+    REF_API int ref_write_fixture_##SUF(const char* path, std::uint32_t rank, const T* d,             \
+                                        std::uint64_t n) {                                            \
+        return guarded([&] { ak::write_fixture<T>(path, rank, std::span<const T>(d, n)); });          \
+    }                                                                                                 \
+    REF_API int ref_read_fixture_##SUF(const char* path, std::uint32_t* rank, T* out,                 \
+                                       std::uint64_t cap, std::uint64_t* n) {                         \
+        return guarded([&] {                                                                          \
+            auto v = ak::read_fixture<T>(path, rank);                                                 \
+            *n = v.size();                                                                            \
+            if (v.size() > cap) throw std::invalid_argument("capacity");                              \
+            std::memcpy(out, v.data(), v.size() * sizeof(T));                                         \
+        });                                                                                           \
+    }
+REF_FIXTURE(i32, std::int32_t)
+REF_FIXTURE(i64, std::int64_t)
+REF_FIXTURE(f32, float)
+REF_FIXTURE(f64, double)
+
+REF_API int ref_emit_csv(const char* path, int nrec, const char* const* case_names, const char* const* dtypes,
+                         const std::uint64_t* n, const std::uint64_t* workers, const std::uint64_t* reps,
+                         const double* mean_ms, const double* stddev_ms, const double* gbps, const double* norm_ms) {
+    return guarded([&] {
+        std::vector<ak::bench::bench_record> recs(nrec);
+        for (int i = 0; i < nrec; ++i) {
+            recs[i].case_name = case_names[i];
+            recs[i].dtype = dtypes[i];
+            recs[i].n = n[i];
+            recs[i].workers = workers[i];
+            recs[i].reps = reps[i];
+            recs[i].mean_ms = mean_ms[i];
+            recs[i].stddev_ms = stddev_ms[i];
+            recs[i].throughput_gbps = gbps[i];
+            recs[i].normalized_ms = norm_ms[i];
+        }
+        ak::bench::emit_csv(std::filesystem::path(path), recs);
+    });
 }

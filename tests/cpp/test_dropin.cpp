@@ -14,6 +14,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ak/reduce.hpp"
@@ -163,7 +164,7 @@ void test_sort() {
 
     // device-resident spans sort in place
     {
-        const std::size_t n = 1 << 20;
+        const std::size_t n = 1 << 19;  // <= k.size()
         void *d = nullptr, *s = nullptr;
         ak::detail::check(ak_malloc(ex.ctx(), n * 8, &d));
         ak::detail::check(ak_malloc(ex.ctx(), n * 8, &s));
@@ -295,13 +296,14 @@ void test_partition() {  // test_exec.cpp:18-22
 }  // namespace
 
 int main() {
-    test_partition();
-    test_reduce();
-    test_accumulate();
-    test_search();
-    test_sort();
-    test_sortperm();
-    test_sihsort();
+    const std::pair<const char*, void (*)()> tests[] = {
+        {"partition", test_partition}, {"reduce", test_reduce},     {"accumulate", test_accumulate},
+        {"search", test_search},       {"sort", test_sort},         {"sortperm", test_sortperm},
+        {"sihsort", test_sihsort}};
+    for (const auto& [name, fn] : tests) {
+        std::fprintf(stderr, "[ run ] %s\n", name);
+        fn();
+    }
     std::printf("test_dropin: %d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
