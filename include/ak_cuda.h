@@ -157,6 +157,37 @@ AK_DECL_SORT(u64, uint64_t)
 AK_DECL_SORT(f32, float)
 AK_DECL_SORT(f64, double)
 
+/* ---- multi-rank reduce / scan over a communicator (the reference has
+ * only single-process reduce.hpp / scan.hpp): local device pass + one allgather of the P rank
+ * partials, folded in rank order; init must be neutral for the op (reduce.hpp:12-14) ---- */
+#define AK_DECL_DIST(S, T)                                                                        \
+    int ak_reduce_all_##S(ak_ctx* ctx, ak_comm* comm, const T* x, uint64_t n, int op, int map,     \
+                          T init, T* host_result);                                                \
+    int ak_accumulate_all_##S(ak_ctx* ctx, ak_comm* comm, const T* x, uint64_t n, T* out,         \
+                              uint64_t out_n, int op, int inclusive, T init);
+AK_DECL_DIST(i32, int32_t)
+AK_DECL_DIST(u32, uint32_t)
+AK_DECL_DIST(i64, int64_t)
+AK_DECL_DIST(u64, uint64_t)
+AK_DECL_DIST(f32, float)
+AK_DECL_DIST(f64, double)
+
+/* ---- any_pred / all_pred (predicates.hpp:57-78): element predicate x OP value with
+ * OP 0 <, 1 <=, 2 >, 3 >=, 4 ==, 5 !=; algo 0 early_exit, 1 via_mapreduce (same result);
+ * *result = 0/1. Empty input: any -> 0, all -> 1 ---- */
+#define AK_DECL_PRED(S, T)                                                                        \
+    int ak_any_pred_##S(ak_ctx* ctx, const T* x, uint64_t n, int op, T value, int algo, int* result); \
+    int ak_all_pred_##S(ak_ctx* ctx, const T* x, uint64_t n, int op, T value, int algo, int* result);
+AK_DECL_PRED(u8, uint8_t)
+AK_DECL_PRED(i8, int8_t)
+AK_DECL_PRED(i16, int16_t)
+AK_DECL_PRED(i32, int32_t)
+AK_DECL_PRED(u32, uint32_t)
+AK_DECL_PRED(i64, int64_t)
+AK_DECL_PRED(u64, uint64_t)
+AK_DECL_PRED(f32, float)
+AK_DECL_PRED(f64, double)
+
 /* ---- communicators (replace sim::world / rank_comm / run_ranks) ---- */
 int ak_nccl_unique_id(void* out, uint64_t bytes /* >= 128 */);
 int ak_comm_nccl_create(const void* unique_id, int nranks, int rank, int device, ak_comm** out);

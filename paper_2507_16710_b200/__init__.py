@@ -581,6 +581,118 @@ class NcclComm:
             self._h = None
 
 
+class LoopbackWorld:
+    """sim::world on one device (sim_comm.hpp:41-80): P logical ranks, each driven by its own
+    host thread with its own ExecBackend; ``comm(r)`` is rank r's rank_comm."""
+
+    def __init__(self, ranks: int):
+        h = C.c_void_p()
+        _check(_fn("ak_world_create", [C.c_int, C.POINTER(C.c_void_p)])(ranks, C.byref(h)))
+        self._h = h
+        self.size = ranks
+
+    def comm(self, rank: int) -> "LoopbackComm":
+        return LoopbackComm(self, rank)
+
+    def abort(self) -> None:
+        _fn("ak_world_abort", [_P])(self._h)
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            if getattr(self, "_h", None):
+                _fn("ak_world_destroy", [_P])(self._h)
+        except Exception:
+            pass
+
+
+class LoopbackComm:
+    def __init__(self, world: LoopbackWorld, rank: int):
+        h = C.c_void_p()
+        _check(_fn("ak_comm_loopback_create", [_P, C.c_int, C.POINTER(C.c_void_p)])(world._h, rank, C.byref(h)))
+        self._h, self.rank, self.size, self._world = h, rank, world.size, world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):  # pragma: no cover
+        try:
+            if getattr(self, "_h", None):
+                _fn("ak_comm_destroy", [_P])(self._h)
+        except Exception:
+            pass
+
+
+def reduce_all(op, data: torch.Tensor, comm, init=None, ex: ExecBackend | None = None, f="identity"):
+    """Reduce over every rank of ``comm``: device pass per rank + one
+    allgather of the rank partials folded in rank order. Collective."""
+    _dev(data, "reduce_all")
+    e = _ex(ex, data)
+    o = _op(op)
+    try:
+        m = _MAPS[f]
+    except (KeyError, TypeError):
+        raise InvalidArgument("map must be identity/abs/square") from None
+    s = _suffix(data)
+    ct = _CT[s]
+    res = ct()
+    if init is None:
+        init = _neutral(data.dtype, o)
+    fn = _fn(f"ak_reduce_all_{s}", [_P, _P, _P, _U64, C.c_int, C.c_int, ct, C.POINTER(ct)])
+    _check(fn(e.handle, comm.handle if comm is not None else None, _ptr(data), data.numel(), o, m, init,
+              C.byref(res)))
+    return res.value
+
+
+def accumulate_all(op, data: torch.Tensor, comm, out: torch.Tensor | None = None, inclusive: bool = True, init=0,
+                   ex: ExecBackend | None = None) -> torch.Tensor:
+    """Prefix scan over the concatenation of every rank's data in rank order: each rank gets its
+    slice of the global scan (local scan seeded with init and the lower ranks' totals). Collective."""
+    _dev(data, "accumulate_all")
+    e = _ex(ex, data)
+    if out is None:
+        out = torch.empty_like(data)
+    s = _suffix(data)
+    ct = _CT[s]
+    fn = _fn(f"ak_accumulate_all_{s}", [_P, _P, _P, _U64, _P, _U64, C.c_int, C.c_int, ct])
+    _check(fn(e.handle, comm.handle if comm is not None else None, _ptr(data), data.numel(), _ptr(out), out.numel(),
+              _op(op), int(inclusive), init))
+    return out
+
+
+_PRED_OPS = {"<": 0, "lt": 0, "<=": 1, "le": 1, ">": 2, "gt": 2, ">=": 3, "ge": 3, "==": 4, "eq": 4, "!=": 5,
+             "ne": 5}
+_PRED_SUFFIX = {**_SUFFIX, torch.uint8: "u8", torch.int8: "i8", torch.int16: "i16"}
+_PRED_CT = dict(_CT, u8=C.c_uint8, i8=C.c_int8, i16=C.c_int16)
+
+
+def _pred(which: str, data: torch.Tensor, op: str, value, ex, algo: str) -> bool:
+    _dev(data, which)
+    e = _ex(ex, data)
+    try:
+        s = _PRED_SUFFIX[data.dtype]
+        o = _PRED_OPS[op]
+    except KeyError:
+        raise InvalidArgument(f"{which}: predicate must be x OP value with OP in < <= > >= == !=") from None
+    if algo not in ("early_exit", "via_mapreduce"):
+        raise InvalidArgument("algo must be early_exit or via_mapreduce")
+    ct = _PRED_CT[s]
+    r = C.c_int()
+    fn = _fn(f"ak_{which}_{s}", [_P, _P, _U64, C.c_int, ct, C.c_int, C.POINTER(C.c_int)])
+    _check(fn(e.handle, _ptr(data), data.numel(), o, value, int(algo == "via_mapreduce"), C.byref(r)))
+    return bool(r.value)
+
+
+def any_pred(data: torch.Tensor, op: str, value, ex: ExecBackend | None = None, algo: str = "early_exit") -> bool:
+    """True iff (x OP value) for some element (predicates.hpp:57-66); empty -> False."""
+    return _pred("any_pred", data, op, value, ex, algo)
+
+
+def all_pred(data: torch.Tensor, op: str, value, ex: ExecBackend | None = None, algo: str = "early_exit") -> bool:
+    """True iff (x OP value) for every element (predicates.hpp:69-78); empty -> True."""
+    return _pred("all_pred", data, op, value, ex, algo)
+
+
 def sihsort(local_data: torch.Tensor, comm: NcclComm | None = None, cfg: SihConfig | None = None,
             ex: ExecBackend | None = None, out: torch.Tensor | None = None, capacity: int | None = None):
     """Distributed sample sort (sihsort.hpp:508-569) of this rank's device keys.

@@ -6,12 +6,14 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <limits>
 #include <type_traits>
 #include <vector>
 
 #include "../../include/ak_cuda.h"
 #include "ctx.cuh"
 #include "radix_sort.cuh"
+#include "predicates.cuh"
 #include "reduce_scan.cuh"
 #include "search_merge.cuh"
 #include "sihsort.cuh"
@@ -337,6 +339,83 @@ void sihsort_loopback_impl(int device, std::uint64_t P, const T* const* in, cons
     if (first) std::rethrow_exception(first);
 }
 
+template <typename T>
+void pred_impl(ak_ctx* c, const T* x, uint64_t n, int op, T v, int any, int algo, int* result) {
+    ctx_lock g(c);
+    need(result != nullptr, "predicate: null result");
+    need(n == 0 || x, "predicate: null input");
+    need(op >= akb::PRED_LT && op <= akb::PRED_NE, "predicate: unknown comparison");
+    const bool found = akb::find_decider<T>(c, x, n, op, v, any != 0, algo == 0);
+    *result = any ? (found ? 1 : 0) : (found ? 0 : 1);  // all(p) = !exists(!p) (predicates.hpp:69-78)
+}
+
+// identity of op for the rank fold (the reference requires a neutral init, reduce.hpp:12-14)
+template <typename T>
+T op_identity(int op) {
+    if (op == akb::OP_SUM) return T(0);
+    if constexpr (std::is_floating_point_v<T>) return op == akb::OP_MIN ? std::numeric_limits<T>::infinity()
+                                                                       : -std::numeric_limits<T>::infinity();
+    else return op == akb::OP_MIN ? std::numeric_limits<T>::max() : std::numeric_limits<T>::lowest();
+}
+template <typename T>
+T op_apply(int op, T a, T b) {
+    if (op == akb::OP_SUM) {
+        if constexpr (std::is_integral_v<T>) {
+            using U = std::make_unsigned_t<T>;
+            return static_cast<T>(static_cast<U>(a) + static_cast<U>(b));
+        } else {
+            return a + b;
+        }
+    }
+    if (op == akb::OP_MIN) return b < a ? b : a;
+    return a < b ? b : a;
+}
+
+// Rank partials: local reduce on the device (identity init), then an allgather.
+template <typename T>
+std::vector<T> rank_partials(ak_ctx* c, akb::comm_iface& cm, const T* x, uint64_t n, int op, int map) {
+    T* dres = reinterpret_cast<T*>(static_cast<char*>(c->small) + 196608 + 128);
+    T local = op_identity<T>(op);
+    if (n) {
+        akb::reduce<T>(c, x, n, op, map, op_identity<T>(op), dres);
+        AKB_CUDA(cudaMemcpyAsync(&local, dres, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+        AKB_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    std::vector<T> all(cm.size());
+    cm.allgather(&local, sizeof(T), all.data());
+    return all;
+}
+
+template <typename T>
+void reduce_all_impl(ak_ctx* c, ak_comm* comm, const T* x, uint64_t n, int op, int map, T init, T* result) {
+    ctx_lock g(c);
+    need(result != nullptr, "reduce_all: null result");
+    need(n == 0 || x, "reduce_all: null input");
+    need(op >= akb::OP_SUM && op <= akb::OP_MAX, "reduce_all: unknown op");
+    self_comm self;
+    akb::comm_iface& cm = comm_of(comm, self, c);
+    const std::vector<T> parts = rank_partials<T>(c, cm, x, n, op, map);
+    T r = init;
+    for (const T& p : parts) r = op_apply<T>(op, r, p);
+    *result = r;
+}
+
+template <typename T>
+void accumulate_all_impl(ak_ctx* c, ak_comm* comm, const T* x, uint64_t n, T* out, uint64_t out_n, int op,
+                         int inclusive, T init) {
+    ctx_lock g(c);
+    need(out_n == n, "accumulate: output length must match input length");  // scan.hpp:32-34
+    need(n == 0 || (x && out), "accumulate_all: null input or output");
+    need(op >= akb::OP_SUM && op <= akb::OP_MAX, "accumulate_all: unknown op");
+    self_comm self;
+    akb::comm_iface& cm = comm_of(comm, self, c);
+    const std::vector<T> parts = rank_partials<T>(c, cm, x, n, op, akb::MAP_IDENTITY);
+    T carry = init;  // init folded with the totals of every lower rank
+    for (int q = 0; q < cm.rank(); ++q) carry = op_apply<T>(op, carry, parts[q]);
+    if (n) akb::scan<T>(c, x, out, n, op, inclusive, carry);
+    akb::ctx_finish(c);
+}
+
 }  // namespace
 
 extern "C" {
@@ -547,6 +626,38 @@ AK_DEFINE(i64, int64_t)
 AK_DEFINE(u64, uint64_t)
 AK_DEFINE(f32, float)
 AK_DEFINE(f64, double)
+
+#define AK_DEFINE_DIST(S, T)                                                                               \
+    int ak_reduce_all_##S(ak_ctx* c, ak_comm* cm, const T* x, uint64_t n, int op, int map, T init, T* r) {    \
+        return guard([&] { reduce_all_impl<T>(c, cm, x, n, op, map, init, r); });                           \
+    }                                                                                                       \
+    int ak_accumulate_all_##S(ak_ctx* c, ak_comm* cm, const T* x, uint64_t n, T* o, uint64_t on, int op,     \
+                              int inc, T init) {                                                            \
+        return guard([&] { accumulate_all_impl<T>(c, cm, x, n, o, on, op, inc, init); });                   \
+    }
+AK_DEFINE_DIST(i32, int32_t)
+AK_DEFINE_DIST(u32, uint32_t)
+AK_DEFINE_DIST(i64, int64_t)
+AK_DEFINE_DIST(u64, uint64_t)
+AK_DEFINE_DIST(f32, float)
+AK_DEFINE_DIST(f64, double)
+
+#define AK_DEFINE_PRED(S, T)                                                                               \
+    int ak_any_pred_##S(ak_ctx* c, const T* x, uint64_t n, int op, T v, int algo, int* r) {                  \
+        return guard([&] { pred_impl<T>(c, x, n, op, v, 1, algo, r); });                                    \
+    }                                                                                                       \
+    int ak_all_pred_##S(ak_ctx* c, const T* x, uint64_t n, int op, T v, int algo, int* r) {                  \
+        return guard([&] { pred_impl<T>(c, x, n, op, v, 0, algo, r); });                                    \
+    }
+AK_DEFINE_PRED(u8, uint8_t)
+AK_DEFINE_PRED(i8, int8_t)
+AK_DEFINE_PRED(i16, int16_t)
+AK_DEFINE_PRED(i32, int32_t)
+AK_DEFINE_PRED(u32, uint32_t)
+AK_DEFINE_PRED(i64, int64_t)
+AK_DEFINE_PRED(u64, uint64_t)
+AK_DEFINE_PRED(f32, float)
+AK_DEFINE_PRED(f64, double)
 
 int ak_nccl_unique_id(void* out, uint64_t bytes) {
     return guard([&] {

@@ -17,6 +17,8 @@
 #include <utility>
 #include <vector>
 
+#include "ak/distributed.hpp"
+#include "ak/predicates.hpp"
 #include "ak/reduce.hpp"
 #include "ak/scan.hpp"
 #include "ak/search.hpp"
@@ -286,6 +288,71 @@ void test_sihsort() {
     }
 }
 
+
+void test_predicates() {  // test_primitives.cpp:206-263 with comparison functors for the lambdas
+    const std::vector<int> zeros(100, 0), ones(100, 1);
+    for (auto algo : {ak::predicate_algo::early_exit, ak::predicate_algo::via_mapreduce}) {
+        CHECK(!ak::any_pred<int>(zeros, ak::pred::gt<int>{0}, ex, algo));
+        CHECK(ak::all_pred<int>(ones, ak::pred::eq<int>{1}, ex, algo));
+        CHECK(!ak::any_pred<int>(std::span<const int>{}, ak::pred::gt<int>{0}, ex, algo));
+        CHECK(ak::all_pred<int>(std::span<const int>{}, ak::pred::gt<int>{0}, ex, algo));
+    }
+    std::mt19937_64 rng(14);
+    std::vector<std::uint8_t> bytes(100000);
+    for (auto& b : bytes) b = (rng() & 0xfff) == 0 ? 1 : 0;  // sparse trues
+    bool want = false;
+    for (auto b : bytes) want = want || b != 0;
+    CHECK(ak::any_pred<std::uint8_t>(bytes, ak::pred::ne<std::uint8_t>{0}, ex) == want);
+    std::mt19937_64 r2(15);
+    for (int inst = 0; inst < 300; ++inst) {
+        const std::size_t n = r2() % 200;
+        const auto data = random_ints<std::int32_t>(r2, n, -10000, 10000);
+        const auto cut = static_cast<std::int32_t>(r2() % 20001) - 10000;
+        bool any = false, all = true;
+        for (auto v : data) {
+            any = any || v < cut;
+            all = all && v < cut;
+        }
+        CHECK(ak::any_pred<std::int32_t>(data, ak::pred::lt<std::int32_t>{cut}, ex) == any);
+        CHECK(ak::all_pred<std::int32_t>(data, ak::pred::lt<std::int32_t>{cut}, ex,
+                                         ak::predicate_algo::via_mapreduce) == all);
+        CHECK(ak::all_pred<std::int32_t>(data, ak::pred::lt<std::int32_t>{cut}, ex) ==
+              !ak::any_pred<std::int32_t>(data, ak::pred::ge<std::int32_t>{cut}, ex));  // duality
+    }
+}
+
+void test_distributed_reduce_scan() {  // 4 ranks on one GPU: slices of the global reduce / scan
+    const std::size_t P = 4;
+    std::mt19937_64 rng(21);
+    std::vector<std::vector<std::int64_t>> parts(P);
+    std::vector<std::int64_t> all;
+    for (std::size_t r = 0; r < P; ++r) {
+        parts[r] = random_ints<std::int64_t>(rng, 10000 + 977 * r, -10000, 10000);
+        all.insert(all.end(), parts[r].begin(), parts[r].end());
+    }
+    std::vector<std::int64_t> scan_all(all.size());
+    std::inclusive_scan(all.begin(), all.end(), scan_all.begin());
+    const std::int64_t total = scan_all.back();
+    std::vector<std::int64_t> sums(P), mins(P);
+    std::vector<std::vector<std::int64_t>> scans(P);
+    ak::sim::world w(P);
+    ak::sim::run_ranks(w, [&](ak::sim::rank_comm& comm) {
+        const auto e = ak::exec_backend::cuda();
+        const auto r = comm.rank();
+        sums[r] = ak::reduce_all<std::int64_t>(ak::plus{}, parts[r], {0, 256}, comm, e);
+        mins[r] = ak::reduce_all<std::int64_t>(ak::minimum{}, parts[r], {std::numeric_limits<std::int64_t>::max(), 256},
+                                               comm, e);
+        scans[r] = ak::accumulate_all<std::int64_t>(ak::plus{}, parts[r], {ak::scan_mode::inclusive, 0, 4096}, comm, e);
+    });
+    std::vector<std::int64_t> cat;
+    for (std::size_t r = 0; r < P; ++r) {
+        CHECK(sums[r] == total);
+        CHECK(mins[r] == *std::min_element(all.begin(), all.end()));
+        cat.insert(cat.end(), scans[r].begin(), scans[r].end());
+    }
+    CHECK(cat == scan_all);
+}
+
 void test_partition() {  // test_exec.cpp:18-22
     CHECK(ak::partition(10, 3) == (std::vector<ak::index_range>{{0, 4}, {4, 7}, {7, 10}}));
     CHECK(ak::partition(2, 5).size() == 2);
@@ -299,7 +366,8 @@ int main() {
     const std::pair<const char*, void (*)()> tests[] = {
         {"partition", test_partition}, {"reduce", test_reduce},     {"accumulate", test_accumulate},
         {"search", test_search},       {"sort", test_sort},         {"sortperm", test_sortperm},
-        {"sihsort", test_sihsort}};
+        {"sihsort", test_sihsort},     {"predicates", test_predicates},
+        {"distributed", test_distributed_reduce_scan}};
     for (const auto& [name, fn] : tests) {
         std::fprintf(stderr, "[ run ] %s\n", name);
         fn();
