@@ -332,7 +332,7 @@ def main():
     dom = max(kernels, key=lambda k: fam[k][0]) if kernels else None
     tr = ncu_traffic(dom)
     names = {"onesweep": "onesweep_kernel (one 8-bit digit pass over all keys)",
-             "local": "local_sort_kernel (on-chip sort of every bucket range, 6 digit passes in smem)",
+             "local": "local_count_kernel (on-chip counting sort of every bucket range; TMA-fed, persistent)",
              "hist": "hist_kernel (top-digit histograms)"}
     roofline = None
     if dom:
@@ -341,15 +341,14 @@ def main():
                     "unit": "GB/s", "frac": kd["frac"], "traffic": (tr * n) if tr else None,
                     "peak_kind": peak_kind, "alg_bytes_per_launch": kd["alg_bytes_per_launch"],
                     "avg_launch_ms": kd["avg_launch_ms"], "launches": fam[dom][1],
-                    "note": ("local_sort_kernel is bound by the shared-memory pipe (ncu l1tex ~90% busy), "
-                             "not HBM: it moves only 16 B/key of HBM traffic for 6 digit passes"
+                    "note": ("local_count_kernel is bound by the shared-memory data pipe (ncu l1tex lsu "
+                             "wavefronts ~70% busy), not HBM: it moves only 16 B/key of HBM traffic"
                              if dom == "local" else None)}
     phases = {k: v[0] / args.steps for k, v in fam.items() if v[1]}
     alg_step = sum(alg_per_key[k] * n * fam[k][1] / args.steps for k in kernels)
     floor_ms = alg_step / (peak * 1e9) * 1e3  # HBM floor of the bytes this algorithm moves
     value = world * n * 8 / 1e9 / (ms / 1e3)
     phases = {k: v[0] / args.steps for k, v in fam.items()}
-    floor_ms = (136 * n) / (peak * 1e9) * 1e3  # local radix sort floor (D=8): 17 passes x 8 B
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

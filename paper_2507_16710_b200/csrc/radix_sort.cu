@@ -134,6 +134,37 @@ __device__ __forceinline__ void red_or_shared(std::uint32_t* addr, std::uint32_t
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// TMA bulk copies (cp.async.bulk, non-tensor) completing on an mbarrier.
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+    asm volatile(
+        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Peer-lane discovery for the warp ranking (AKB_MATCH selects at run time):
 enum match_kind : int { MATCH_BALLOT = 0, MATCH_HW = 1, MATCH_SMEM = 2, MATCH_HYBRID = 3, MATCH_HALF = 4 };
 
@@ -753,27 +784,27 @@ struct local_smem {
     static constexpr std::size_t total = red_off + 2 * LOCAL_WARPS * sizeof(std::uint64_t);
 };
 
+// Stable on-chip sort of range `range` (cuts[range] .. cuts[range+1]); see above.
 template <typename T, int ITEMS>
-__global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3 : 2))
-    local_sort_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
-                      int desc, int low, std::uint64_t* big) {
+__device__ __forceinline__ void local_radix_range(const T* __restrict__ in, T* __restrict__ out,
+                                                  const std::uint64_t* __restrict__ cuts, std::uint64_t range,
+                                                  int desc, int low, std::uint64_t* big, unsigned char* smem) {
     using L = local_smem<T, ITEMS>;
     using B = typename key_traits<T>::bits;
     constexpr int CAP = LOCAL_BLOCK * ITEMS;
     constexpr int PASSES = key_traits<T>::nbits / 8;
-    extern __shared__ __align__(16) unsigned char smem[];
     T* s_stage = reinterpret_cast<T*>(smem + L::stage_off);
     std::uint32_t* s_tab = reinterpret_cast<std::uint32_t*>(smem + L::tab_off);
     std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
     B* s_red = reinterpret_cast<B*>(smem + L::red_off);
     std::uint32_t* s_maxrun = s_wsum + 8;
 
-    const std::uint64_t b = cuts[blockIdx.x], e = cuts[blockIdx.x + 1];
+    const std::uint64_t b = cuts[range], e = cuts[range + 1];
     if (b >= e) return;
     if (e - b > static_cast<std::uint64_t>(CAP)) {  // left for the segment fallback
         if (threadIdx.x == 0) {
             const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
-            big[1 + slot] = blockIdx.x;
+            big[1 + slot] = range;
         }
         return;
     }
@@ -989,6 +1020,345 @@ __global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3
     for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) out[b + j] = s_stage[j];
 }
 
+// One CTA per range.
+template <typename T, int ITEMS>
+__global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3 : 2))
+    local_sort_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
+                      int desc, int low, std::uint64_t* big) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    local_radix_range<T, ITEMS>(in, out, cuts, blockIdx.x, desc, low, big, smem);
+}
+
+// Persistent loop over the ranges listed in list[1 .. list[0]] (the ranges the counting
+// kernel below handed back).
+template <typename T, int ITEMS>
+__global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3 : 2))
+    local_redo_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
+                      int desc, int low, std::uint64_t* big, const std::uint64_t* __restrict__ list) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const std::uint64_t nr = list[0];
+    for (std::uint64_t r = blockIdx.x; r < nr; r += gridDim.x) {
+        local_radix_range<T, ITEMS>(in, out, cuts, list[1 + r], desc, low, big, smem);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Keys-only integer ranges: on-chip COUNTING sort (stability is unobservable for
+// integer keys without payload -- equal keys are identical bit patterns -- so the
+// order of equal digits may be arbitrary). One CTA per range:
+//   1. load the range (coalesced), OR/AND-reduce the ordered keys -> varying bits;
+//   2. bin by the top nb varying bits (2^nb ~ len bins, Poisson(~1) keys per bin):
+//      one shared atomic per key gives its slot inside the bin;
+//   3. block scan of the bin counts -> bin starts; keys stored at start + slot;
+//   4. each key ranks itself inside its (short) bin on the full key and is written
+//      straight to its final global position (bins are contiguous, so a warp's
+//      stores stay within a few sectors).
+// A range whose fullest bin exceeds LC_MAX_BIN (clustered keys) is left untouched and
+// listed in `redo` for the stable radix kernel above.
+// ---------------------------------------------------------------------------
+// 1 if (a, ia) < (b, ib) lexicographically (64-bit unsigned key, then 32-bit index): the
+// borrow out of the 96-bit subtraction -- four integer ops, no compares or branches.
+__device__ __forceinline__ std::uint32_t lex_less96(std::uint64_t a, std::uint32_t ia, std::uint64_t b,
+                                                    std::uint32_t ib) {
+    std::uint32_t d0, d1, d2, bor;
+    asm("sub.cc.u32 %0, %4, %5;\n\t"
+        "subc.cc.u32 %1, %6, %7;\n\t"
+        "subc.cc.u32 %2, %8, %9;\n\t"
+        "subc.u32 %3, 0, 0;"
+        : "=r"(d0), "=r"(d1), "=r"(d2), "=r"(bor)
+        : "r"(ia), "r"(ib), "r"(static_cast<std::uint32_t>(a)), "r"(static_cast<std::uint32_t>(b)),
+          "r"(static_cast<std::uint32_t>(a >> 32)), "r"(static_cast<std::uint32_t>(b >> 32)));
+    return bor & 1u;
+}
+
+constexpr int LC_BLOCK = 512;
+constexpr int LC_WARPS = LC_BLOCK / 32;
+constexpr int LC_MAX_BITS = 13;                        // up to 8192 bins (u16 counts, 2 per word)
+constexpr int LC_WORDS = (1 << LC_MAX_BITS) / 2;       // 4096 counter words = 16 KB
+constexpr std::uint32_t LC_MAX_BIN = 48;
+#ifndef AKB_LC_EXTRA
+#define AKB_LC_EXTRA 1  // bins = 2^(ceil(log2(len)) + EXTRA): ~2 bins per key
+#endif
+
+template <typename T, int ITEMS>
+struct lc_smem {
+    static constexpr int CAP = LC_BLOCK * ITEMS;
+    // two key buffers (the range being sorted + the next range in flight), each with one
+    // spare key at both ends: TMA copies the 16-byte aligned superset of a range
+    static constexpr std::size_t buf_bytes = (sizeof(T) * (CAP + 2) + 15) & ~std::size_t(15);
+    static constexpr std::size_t buf_off = 0;
+    static constexpr std::size_t cnt_off = 2 * buf_bytes;
+    static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LC_WORDS + 4);
+    static constexpr std::size_t side_off = cnt_off + cnt_bytes;  // u16 per staged key: slot | bin size << 8
+    static constexpr std::size_t side_bytes = (sizeof(std::uint16_t) * CAP + 15) & ~std::size_t(15);
+    static constexpr std::size_t red_off = side_off + side_bytes;  // 2 x WARPS x u64 or/and partials
+    static constexpr std::size_t wsum_off = red_off + 2 * LC_WARPS * sizeof(std::uint64_t);
+    static constexpr std::size_t bar_off = wsum_off + 2 * LC_WARPS * sizeof(std::uint32_t);
+    static constexpr std::size_t total = bar_off + 2 * sizeof(std::uint64_t);
+    static constexpr int MINB = total + 1024 <= 114 * 1024 ? 2 : 1;  // CTAs per SM that fit
+};
+
+// Keys-only 64-bit integer ranges: on-chip COUNTING sort. Stability is unobservable for
+// integer keys without payload (equal keys are identical bit patterns), so the order in
+// which equal bins fill may be arbitrary. Persistent CTAs walk the ranges; a range's keys
+// arrive by one TMA bulk copy (cp.async.bulk + mbarrier) issued while the previous range is
+// being sorted. Per range:
+//   1. OR/AND-reduce the keys -> varying bits; bin = the top nb varying bits (~2 bins per key);
+//   2. one shared atomic per key on its bin's packed u16 counter gives its slot in the bin;
+//   3. scan of the counters -> bin starts; keys stored at start + slot (bin order);
+//   4. each staged position ranks its key inside its (short) bin on the full key and stores
+//      it to out[b + rank] (nearly coalesced: rank stays inside the bin).
+// A range whose fullest bin exceeds LC_MAX_BIN (clustered keys) is left untouched and listed
+// in `redo` for the stable radix kernel; ranges above CAP go to `big` (segment fallback).
+template <typename T, int ITEMS, bool DESC>
+__global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
+    local_count_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
+                       std::uint64_t J, std::uint64_t* big, std::uint64_t* redo) {
+    using L = lc_smem<T, ITEMS>;
+    using B = typename key_traits<T>::bits;
+    constexpr int CAP = L::CAP;
+    static_assert(sizeof(T) == 8, "TMA alignment math assumes 8-byte keys");
+    extern __shared__ __align__(16) unsigned char smem[];
+    std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + L::cnt_off);  // packed u16 counts
+    std::uint16_t* s_c16 = reinterpret_cast<std::uint16_t*>(smem + L::cnt_off);
+    std::uint16_t* s_side = reinterpret_cast<std::uint16_t*>(smem + L::side_off);
+    B* s_red = reinterpret_cast<B*>(smem + L::red_off);
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    std::uint64_t* s_bar = reinterpret_cast<std::uint64_t*>(smem + L::bar_off);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // TMA needs a 16-byte aligned source; the copy is the 16-byte aligned superset of the
+    // range, which never leaves the allocation's last 16-byte granule
+    const bool tma = (reinterpret_cast<std::uintptr_t>(in) & 15) == 0;
+    auto fits = [&](std::uint64_t rb, std::uint64_t re) {
+        return re > rb && re - rb <= static_cast<std::uint64_t>(CAP);
+    };
+    auto issue = [&](std::uint64_t r, int q) {  // one thread
+        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
+        if (!tma || !fits(rb, re)) return;
+        const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
+        const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
+        mbar_arrive_expect_tx(s_bar + q, bytes);
+        bulk_g2s(smem + L::buf_off + q * L::buf_bytes, in + a0, bytes, s_bar + q);
+    };
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        mbar_init(s_bar + 1, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    if (tid == 0 && blockIdx.x < J) issue(blockIdx.x, 0);
+    std::uint32_t ph0 = 0, ph1 = 0;  // parity of each buffer's next completion
+
+#pragma unroll 1
+    for (std::uint64_t r = blockIdx.x, it = 0; r < J; r += gridDim.x, ++it) {
+        const int cur = static_cast<int>(it & 1);
+        T* s_stage = reinterpret_cast<T*>(smem + L::buf_off + cur * L::buf_bytes);
+        const std::uint64_t b = cuts[r], e = cuts[r + 1];
+        const bool ok_range = fits(b, e);
+        const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
+        const std::uint32_t off = static_cast<std::uint32_t>(b & 1);
+        if (ok_range && tma) {
+            if (cur) {
+                mbar_wait(s_bar + 1, ph1);
+                ph1 ^= 1u;
+            } else {
+                mbar_wait(s_bar, ph0);
+                ph0 ^= 1u;
+            }
+        }
+
+        // keys -> registers; varying bits. XOR with a constant (sign flip, descending
+        // complement) flips a bit in every key alike, so OR & ~AND of the raw bits equals
+        // that of the ordered bits. Padding repeats key 0 (neutral for OR/AND).
+        T k[ITEMS];
+        B orv = 0, andv = static_cast<B>(~B(0));
+        if (len) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const std::uint32_t li = static_cast<std::uint32_t>(i * LC_BLOCK + tid);
+                const std::uint32_t lj = li < len ? li : 0u;
+                k[i] = tma ? s_stage[lj + off] : in[b + lj];
+                orv |= static_cast<B>(k[i]);
+                andv &= static_cast<B>(k[i]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            orv |= __shfl_xor_sync(FULL, orv, o);
+            andv &= __shfl_xor_sync(FULL, andv, o);
+        }
+        if (lane == 0) {
+            s_red[warp] = orv;
+            s_red[LC_WARPS + warp] = andv;
+        }
+        const int nb_want = min(LC_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
+        const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
+        if (nwords_w >= 4) {
+            for (int i = tid; i < nwords_w / 4; i += LC_BLOCK)
+                reinterpret_cast<uint4*>(s_cw)[i] = make_uint4(0, 0, 0, 0);
+        } else if (tid < nwords_w) {
+            s_cw[tid] = 0;
+        }
+        fence_proxy_async_smem();  // generic accesses to the other buffer precede its next TMA write
+        __syncthreads();
+        // every thread is past the previous range: its buffer may take the next one
+        if (tid == 0 && r + gridDim.x < J) issue(r + gridDim.x, cur ^ 1);
+        if (!ok_range) {
+            if (e - b > static_cast<std::uint64_t>(CAP) && tid == 0) {  // left for the segment fallback
+                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+                big[1 + slot] = r;
+            }
+            __syncthreads();  // s_red is rewritten by the next range
+            continue;
+        }
+        B any1 = 0, all1 = static_cast<B>(~B(0));
+#pragma unroll
+        for (int w = 0; w < LC_WARPS; ++w) {
+            any1 |= s_red[w];
+            all1 &= s_red[LC_WARPS + w];
+        }
+        const B vary = any1 & ~all1;
+        if (vary == 0) {  // every key equal: the range is already sorted
+            if (in != out)
+                for (std::uint32_t j = tid; j < len; j += LC_BLOCK) out[b + j] = k[0];
+            __syncthreads();
+            continue;
+        }
+        int hb;
+        if constexpr (sizeof(B) == 8) hb = 63 - __clzll(static_cast<long long>(vary));
+        else hb = 31 - __clz(static_cast<int>(vary));
+        const int nb = max(1, min(nb_want, hb + 1));
+        const int shift = hb + 1 - nb;
+        const std::uint32_t bmask = (1u << nb) - 1u;
+        const std::uint32_t nwords = 1u << (nb - 1);
+
+        // bin | slot << 16 per key: one shared atomic per key on its bin's half of a word
+        std::uint32_t pk[ITEMS];
+        bool over = false;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const bool ok = static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len;
+            const std::uint32_t bn = static_cast<std::uint32_t>(ordered(k[i], DESC) >> shift) & bmask;
+            const std::uint32_t sh = (bn & 1u) * 16u;
+            const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
+            const std::uint32_t slot = (old >> sh) & 0xffffu;
+            over |= ok && slot >= LC_MAX_BIN;
+            pk[i] = bn | (slot << 16);
+        }
+        if (__syncthreads_or(over)) {  // clustered keys: hand the range to the radix kernel
+            if (tid == 0) {
+                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(redo), 1ull);
+                redo[1 + slot] = r;
+            }
+            continue;
+        }
+        // exclusive scan of the packed counts -> packed u16 bin starts. Warp w owns words
+        // [w*WPW, (w+1)*WPW), lane l the uint4 quads q*128 + 4l (conflict-free), order (q, lane).
+        {
+            const std::uint32_t wpw = nwords / LC_WARPS;  // words per warp (0 when nwords < 16)
+            const std::uint32_t nq = wpw / 128;           // full quads per lane
+            std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
+            if (nq >= 1) {
+                // up to 2 quads per lane (LC_WORDS / LC_WARPS = 256 words = 2 x 128)
+                uint4 u[2];
+                std::uint32_t cs[2] = {0, 0};
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (q < static_cast<int>(nq)) {
+                        u[q] = *reinterpret_cast<const uint4*>(wbase + q * 128);
+                        const std::uint32_t S = u[q].x + u[q].y + u[q].z + u[q].w;
+                        cs[q] = (S & 0xffffu) + (S >> 16);
+                    }
+                std::uint32_t p = cs[0] | (cs[1] << 16);  // both quads' sums scanned at once
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const std::uint32_t y = __shfl_up_sync(FULL, p, o);
+                    if (lane >= o) p += y;
+                }
+                const std::uint32_t t = __shfl_sync(FULL, p, 31);
+                const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
+                if (lane == 0) s_wsum[warp] = T0 + T1;
+                __syncthreads();
+                std::uint32_t wp = 0;
+#pragma unroll
+                for (int w = 0; w < LC_WARPS; ++w) wp += w < warp ? s_wsum[w] : 0u;
+                const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (q < static_cast<int>(nq)) {
+                        std::uint32_t run = exq[q];
+                        std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u[q]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
+                            wv[j] = run | ((run + lo) << 16);
+                            run += lo + hi;
+                        }
+                        *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
+                    }
+            } else {
+                // small tables (<= 1024 words): thread t owns words [wpt*t, wpt*t + wpt), wpt <= 2
+                const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
+                const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
+                const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
+                const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
+                const std::uint32_t S = c0 + c1;
+                const std::uint32_t sum = (S & 0xffffu) + (S >> 16);
+                std::uint32_t inc = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                if (lane == 31) s_wsum[warp] = inc;
+                __syncthreads();
+                std::uint32_t wp = 0;
+#pragma unroll
+                for (int w = 0; w < LC_WARPS; ++w) wp += w < warp ? s_wsum[w] : 0u;
+                std::uint32_t run = wp + inc - sum;
+                if (w0 < nwords) {
+                    const std::uint32_t lo = c0 & 0xffffu, hi = c0 >> 16;
+                    s_cw[w0] = run | ((run + lo) << 16);
+                    run += lo + hi;
+                }
+                if (wpt == 2 && w0 + 1 < nwords) s_cw[w0 + 1] = run | ((run + (c1 & 0xffffu)) << 16);
+            }
+            if (tid == 0) s_c16[2 * nwords] = static_cast<std::uint16_t>(len);  // end of the last bin
+        }
+        __syncthreads();
+        // scatter into bin order; side[staged slot] = slot in bin | bin size << 8
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len) {
+                const std::uint32_t bn = pk[i] & 0xffffu, slot = pk[i] >> 16;
+                const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
+                reinterpret_cast<B*>(s_stage)[st + slot] = ordered(k[i], DESC);  // ranked as unsigned bits
+                s_side[st + slot] = static_cast<std::uint16_t>(slot | (cnt << 8));
+            }
+        }
+        __syncthreads();
+        // each staged position ranks its key inside its (short) bin on the full key:
+        // final slot = bin start + #(key, staged slot) lexicographically smaller
+        B* s_ord = reinterpret_cast<B*>(s_stage);
+#pragma unroll 1
+        for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
+            const B v = s_ord[x];
+            const std::uint32_t sd = s_side[x];
+            const std::uint32_t cnt = sd >> 8;
+            std::uint32_t rk = x;
+            if (cnt > 1) {
+                const std::uint32_t st = x - (sd & 0xffu);
+                rk = st + lex_less96(s_ord[st], st, v, x) + lex_less96(s_ord[st + 1], st + 1, v, x);
+#pragma unroll 1
+                for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(s_ord[y], y, v, x);
+            }
+            const B o = DESC ? static_cast<B>(~v) : v;
+            out[b + rk] = static_cast<T>(std::is_signed_v<T> ? (o ^ (B(1) << (8 * sizeof(B) - 1))) : o);
+        }
+    }  // ranges
+}
+
 // cut j = first index of the bucket (top bits) holding position j*step; cuts[J] = n.
 template <typename T>
 __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
@@ -1059,6 +1429,48 @@ void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std
     c->kernel_launches += 1;
 }
 
+int local_count_env() {
+    static const int v = [] {
+        const char* e = std::getenv("AKB_LOCAL_COUNT");  // "0": stable radix local stage for every range
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+// Counting local stage (integer keys only), then the stable radix kernel over the ranges
+// it handed back (persistent loop over redo[1 .. redo[0]]; no host round trip).
+template <typename T, int ITEMS>
+void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, std::uint64_t n,
+                        bool desc, int low, std::uint64_t* big, std::uint64_t* redo) {
+    constexpr int CITEMS = ITEMS * LOCAL_BLOCK / LC_BLOCK;
+    static_assert(CITEMS * LC_BLOCK == ITEMS * LOCAL_BLOCK, "same range capacity");
+    using CS = lc_smem<T, CITEMS>;
+    using LS = local_smem<T, ITEMS>;
+    static bool configured = false;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(local_count_kernel<T, CITEMS, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CS::total)));
+        AKB_CUDA(cudaFuncSetAttribute(local_count_kernel<T, CITEMS, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CS::total)));
+        AKB_CUDA(cudaFuncSetAttribute(local_redo_kernel<T, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(LS::total)));
+        configured = true;
+    }
+    AKB_CUDA(cudaMemsetAsync(redo, 0, sizeof(std::uint64_t), c->stream));
+    const int tok = ctx_prof_begin(c, KF_LOCAL);
+    const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * CS::MINB));
+    if (desc)
+        local_count_kernel<T, CITEMS, true><<<grid, LC_BLOCK, CS::total, c->stream>>>(G, kout, cuts, J, big, redo);
+    else
+        local_count_kernel<T, CITEMS, false><<<grid, LC_BLOCK, CS::total, c->stream>>>(G, kout, cuts, J, big, redo);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    local_redo_kernel<T, ITEMS><<<static_cast<unsigned>(c->sm_count * 2), LOCAL_BLOCK, LS::total, c->stream>>>(
+        G, kout, cuts, desc ? 1 : 0, low, big, redo);
+    AKB_CUDA(cudaGetLastError());
+    c->kernel_launches += 2;
+}
+
 // Returns false when the plain LSD should be used instead.
 //
 // The plan is read off the data: one histogram pass over the top three digits (plus all
@@ -1068,7 +1480,7 @@ void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std
 // buckets fit a CTA is taken. Skewed inputs thus get more global digits instead of
 // oversized ranges; a mis-estimate only costs the (bounded) segment fallback.
 template <typename T>
-bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
+bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
     constexpr int PASSES = key_traits<T>::nbits / 8;
     const int env = hybrid_env();
     // 64-bit integer keys. Float keys concentrate their top digits in the exponent (uniform
@@ -1173,8 +1585,9 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
         }
         G = cur;
     }
-    std::uint64_t* cuts = ctx_cuts(c, 2 * J + 3);
+    std::uint64_t* cuts = ctx_cuts(c, 3 * J + 4);
     std::uint64_t* big = cuts + J + 1;
+    std::uint64_t* redo = big + J + 1;
     AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
     const int top_shift = 8 * (top - (m > 0 ? m : 1));
     if (bucket_mode)
@@ -1190,7 +1603,17 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
     int low = top - m - 2;
     if (low < 0) low = 0;
     if (const char* e = std::getenv("AKB_LOCAL_LOW")) low = std::atoi(e);
-    if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, low, big);
+    bool counted = false;
+    if constexpr (std::is_integral_v<T> && sizeof(T) == 8) {  // the only keys that reach here (see above)
+        if (local_count_env() != 0) {
+            if (items == 8) launch_local_count<T, 8>(c, G, kout, cuts, J, n, desc, low, big, redo);
+            else if (items == 12) launch_local_count<T, 12>(c, G, kout, cuts, J, n, desc, low, big, redo);
+            else launch_local_count<T, 16>(c, G, kout, cuts, J, n, desc, low, big, redo);
+            counted = true;
+        }
+    }
+    if (counted) {
+    } else if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, low, big);
     else if (items == 12) launch_local<T, 12>(c, G, kout, cuts, J, desc, low, big);
     else launch_local<T, 16>(c, G, kout, cuts, J, desc, low, big);
     if (m == 0) return true;  // a single range of <= LOCAL_TILE keys always fits
@@ -1222,6 +1645,12 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
         }
     }
     return true;
+}
+
+template <typename T>
+bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
+    if constexpr (std::is_integral_v<T> && sizeof(T) == 8) return hybrid_sort_keys_impl<T>(c, kin, kout, kalt, n, desc);
+    else return false;
 }
 
 }  // namespace
