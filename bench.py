@@ -278,7 +278,7 @@ def main():
     ms_local = e0.elapsed_time(e1) / args.steps
     gpu_launches = ex.kernel_launches() - launches0
     ex.set_profiling(False)
-    fam = {k: ex.kernel_time(k) for k in ("onesweep", "local", "hist", "merge", "exchange", "search", "other")}
+    fam = {k: ex.kernel_time(k) for k in ("msd", "onesweep", "local", "hist", "merge", "exchange", "search", "other")}
     ms = ms_local
     if comm is not None:
         ms = comm.allreduce_max([ms_local], ex)[0]
@@ -320,7 +320,7 @@ def main():
     # Algorithmic HBM bytes per launch of each kernel family:
     # a onesweep digit pass and the on-chip range sort each read and write every key once
     # (16 B/key), the top-digit histogram reads every key once (8 B/key).
-    alg_per_key = {"onesweep": 16, "local": 16, "hist": 8}
+    alg_per_key = {"msd": 16, "onesweep": 16, "local": 16, "hist": 8}
     kernels = {}
     for k, per_key in alg_per_key.items():
         t_ms, cnt = fam[k]
@@ -331,7 +331,8 @@ def main():
                           "alg_bytes_per_launch": per_key * n, "achieved_gbs": ach, "frac": ach / peak}
     dom = max(kernels, key=lambda k: fam[k][0]) if kernels else None
     tr = ncu_traffic(dom)
-    names = {"onesweep": "onesweep_kernel (one 8-bit digit pass over all keys)",
+    names = {"msd": "msd_pass_kernel (unstable top-digit partition pass over all keys; per-bin atomic cursors)",
+             "onesweep": "onesweep_kernel (one 8-bit digit pass over all keys)",
              "local": "local_count_kernel (on-chip counting sort of every bucket range; TMA-fed, persistent)",
              "hist": "hist_kernel (top-digit histograms)"}
     roofline = None

@@ -76,7 +76,8 @@ void* ak_ctx_stream(const ak_ctx* ctx);
  * (bench.py's live roofline). Families: */
 enum { AK_KF_ONESWEEP = 0, AK_KF_HIST = 1, AK_KF_MERGE = 2, AK_KF_REDUCE = 3, AK_KF_SCAN = 4,
        AK_KF_SEARCH = 5, AK_KF_EXCHANGE = 6, AK_KF_OTHER = 7,
-       AK_KF_LOCAL = 8 /* hybrid sort: on-chip range sort */ };
+       AK_KF_LOCAL = 8 /* hybrid sort: on-chip range sort */,
+       AK_KF_MSD = 9 /* hybrid sort: unstable top-digit partition passes */ };
 int ak_ctx_set_profiling(ak_ctx* ctx, int on);
 /* synchronises the stream, then reports accumulated ms and launch count */
 int ak_ctx_kernel_time(ak_ctx* ctx, int family, double* ms, uint64_t* launches);

@@ -185,7 +185,7 @@ class ExecBackend:
         return int(_lib.ak_ctx_kernel_launches(self._h))
 
     KF = {"onesweep": 0, "hist": 1, "merge": 2, "reduce": 3, "scan": 4, "search": 5, "exchange": 6,
-          "other": 7, "local": 8}
+          "other": 7, "local": 8, "msd": 9}
 
     def set_profiling(self, on: bool) -> None:
         """Bracket every hot kernel with CUDA events on the ctx stream."""

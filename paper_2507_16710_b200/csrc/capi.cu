@@ -456,6 +456,7 @@ int ak_ctx_destroy(ak_ctx* c) {
         if (c->small) cudaFree(c->small);
         if (c->split) cudaFree(c->split);
         if (c->cuts) cudaFree(c->cuts);
+        if (c->msd) cudaFree(c->msd);
         if (c->stage) cudaFree(c->stage);
         if (c->pinned) cudaFreeHost(c->pinned);
         for (auto& t : c->pending) {
@@ -502,7 +503,7 @@ int ak_ctx_set_profiling(ak_ctx* c, int on) {
 int ak_ctx_kernel_time(ak_ctx* c, int family, double* ms, uint64_t* launches) {
     return guard([&] {
         ctx_lock g(c);
-        need(family >= 0 && family < 9, "ak_ctx_kernel_time: bad family");
+        need(family >= 0 && family < 10, "ak_ctx_kernel_time: bad family");
         AKB_CUDA(cudaStreamSynchronize(c->stream));
         akb::ctx_prof_resolve(c);
         if (ms) *ms = c->family_ms[family];

@@ -148,6 +148,11 @@ std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count) {
     return c->cuts;
 }
 
+std::uint64_t* ctx_msd(ak_ctx* c) {
+    if (!c->msd) AKB_CUDA(cudaMalloc(&c->msd, (2 * 65536 + 256) * sizeof(std::uint64_t)));
+    return c->msd;
+}
+
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count) {
     if (count > c->split_cap) {
         if (c->split) {

@@ -53,6 +53,9 @@ struct ak_ctx {
     std::uint64_t* cuts = nullptr;
     std::size_t cuts_cap = 0;
 
+    // hybrid radix sort, MSD passes: 16-bit joint histogram + 16-bit / 8-bit bucket cursors
+    std::uint64_t* msd = nullptr;
+
     // device staging for the *_host entry points (end-to-end path)
     void* stage = nullptr;
     std::size_t stage_bytes = 0;
@@ -100,11 +103,13 @@ void ctx_finish(ak_ctx* c);  // synchronise when blocking
 void* ctx_pinned(ak_ctx* c, std::size_t bytes);
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count);
 std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count);
+// MSD-pass tables: [65536 joint counts][65536 16-bit cursors][256 8-bit cursors]
+std::uint64_t* ctx_msd(ak_ctx* c);
 void* ctx_stage(ak_ctx* c, std::size_t bytes);
 
 // Kernel families for ak_ctx_kernel_time (C ABI: AK_KF_*).
 enum kernel_family : int { KF_ONESWEEP = 0, KF_HIST = 1, KF_MERGE = 2, KF_REDUCE = 3, KF_SCAN = 4,
-                           KF_SEARCH = 5, KF_EXCHANGE = 6, KF_OTHER = 7, KF_LOCAL = 8 };
+                           KF_SEARCH = 5, KF_EXCHANGE = 6, KF_OTHER = 7, KF_LOCAL = 8, KF_MSD = 9 };
 // Bracket one launch with events when profiling is on (returns -1 when off).
 int ctx_prof_begin(ak_ctx* c, int family);
 void ctx_prof_end(ak_ctx* c, int token);

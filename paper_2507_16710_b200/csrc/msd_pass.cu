@@ -1,0 +1,341 @@
+// msd_pass.cu -- unstable MSD partition passes for keys-only 64-bit integer sorts.
+//
+// For keys without payload, stability is unobservable (equal integer keys are identical
+// bit patterns), so the global top-digit passes of the hybrid sort need no look-back
+// chain: a tile claims its output space per bin with one global atomicAdd on that bin's
+// cursor, whose start comes from a histogram computed in the single upfront read.
+//
+//   hist_joint_kernel: one read of the keys -> the 256-bin histograms of the top three
+//       digits (the plan) and the 65536-bin histogram of the top 16 bits (the cursors);
+//   joint_scan_kernel: exclusive scan of the 65536 counts -> 16-bit bucket starts and the
+//       8-bit bucket starts (the cursors of both passes);
+//   msd_pass_kernel<LEVEL>: LEVEL 1 partitions by the top 8 bits, LEVEL 2 partitions each
+//       top-8 bucket by the next 8 bits (a tile of the LEVEL-1 output spans few top
+//       buckets). Per tile: load (128-bit, coalesced) -> shared-atomic slots per bin ->
+//       bin starts + one global atomicAdd per non-empty bin -> keys staged in bin order
+//       in shared memory -> contiguous per-bin runs written out.
+// After the two passes the array is ordered by its top 16 bits, exactly as the stable
+// top-digit onesweep passes leave it up to the order inside each 16-bit bucket, which the
+// local stage sorts anyway.
+#include <cstdint>
+
+#include "msd_pass.cuh"
+
+namespace akb {
+
+namespace {
+
+constexpr std::uint32_t FULLM = 0xffffffffu;
+constexpr int JOINT_BITS = 16;
+constexpr int JOINT_BINS = 1 << JOINT_BITS;
+constexpr int JH_BLOCK = 1024;
+constexpr int JH_PARTS = 4;
+constexpr std::uint32_t JH_FLUSH = 0x4000;  // u16 half-counter spill threshold
+
+template <typename T>
+__device__ __forceinline__ std::uint64_t ord64(T v, bool desc) {
+    return static_cast<std::uint64_t>(ordered(v, desc));
+}
+
+// Joint histogram: 65536 u16 counters packed two per shared word (128 KB). A counter that
+// reaches JH_FLUSH is moved to the global histogram by the thread whose increment reached
+// it (at most JH_BLOCK increments can be in flight, far below the 0x10000 - JH_FLUSH of
+// headroom, so a half never carries into its neighbour).
+template <typename T>
+__global__ void __launch_bounds__(JH_BLOCK, 1)
+    hist_joint_kernel(const T* __restrict__ keys, std::uint64_t n, int desc, std::uint64_t* __restrict__ g_hist,
+                      std::uint64_t* __restrict__ g_joint) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    std::uint32_t* s_joint = reinterpret_cast<std::uint32_t*>(smem);                    // 32768 words
+    std::uint32_t* s_dig = reinterpret_cast<std::uint32_t*>(smem + JOINT_BINS * 2);      // 256 x PARTS
+    for (int i = threadIdx.x; i < JOINT_BINS / 2; i += JH_BLOCK) s_joint[i] = 0;
+    for (int i = threadIdx.x; i < 256 * JH_PARTS; i += JH_BLOCK) s_dig[i] = 0;
+    __syncthreads();
+    const bool dsc = desc != 0;
+    const int part = threadIdx.x % JH_PARTS;
+    auto count = [&](T k) {
+        const std::uint64_t o = ord64(k, dsc);
+        const std::uint32_t hi = static_cast<std::uint32_t>(o >> 32);
+        atomicAdd(&s_dig[((hi >> 8) & 0xffu) * JH_PARTS + part], 1u);  // digit 5 (digits 6, 7: marginals)
+        const std::uint32_t bin = hi >> 16;
+        const std::uint32_t sh = (bin & 1u) * 16u;
+        const std::uint32_t old = atomicAdd(&s_joint[bin >> 1], 1u << sh);
+        if (((old >> sh) & 0xffffu) == JH_FLUSH - 1) {
+            atomicSub(&s_joint[bin >> 1], JH_FLUSH << sh);
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_joint + bin), static_cast<unsigned long long>(JH_FLUSH));
+        }
+    };
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * JH_BLOCK;
+    const std::uint64_t tid = static_cast<std::uint64_t>(blockIdx.x) * JH_BLOCK + threadIdx.x;
+    std::uint64_t done = 0;
+    if ((reinterpret_cast<std::uintptr_t>(keys) & 15) == 0) {
+        const std::uint64_t nv = n / 2;
+        const uint4* kv = reinterpret_cast<const uint4*>(keys);
+        std::uint64_t i = tid;
+        for (; i + 3 * stride < nv; i += 4 * stride) {
+            uint4 a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = __ldg(kv + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                count(reinterpret_cast<const T*>(&a[u])[0]);
+                count(reinterpret_cast<const T*>(&a[u])[1]);
+            }
+        }
+        for (; i < nv; i += stride) {
+            const uint4 a = __ldg(kv + i);
+            const T* e = reinterpret_cast<const T*>(&a);
+            count(e[0]);
+            count(e[1]);
+        }
+        done = nv * 2;
+    }
+    for (std::uint64_t i = done + tid; i < n; i += stride) count(keys[i]);
+    __syncthreads();
+    for (int w = threadIdx.x; w < JOINT_BINS / 2; w += JH_BLOCK) {
+        const std::uint32_t v = s_joint[w];
+        if (v & 0xffffu)
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_joint + 2 * w), static_cast<unsigned long long>(v & 0xffffu));
+        if (v >> 16)
+            atomicAdd(reinterpret_cast<unsigned long long*>(g_joint + 2 * w + 1), static_cast<unsigned long long>(v >> 16));
+    }
+    for (int i = threadIdx.x; i < 256; i += JH_BLOCK) {
+        std::uint32_t s = 0;
+#pragma unroll
+        for (int q = 0; q < JH_PARTS; ++q) s += s_dig[i * JH_PARTS + q];
+        if (s) atomicAdd(reinterpret_cast<unsigned long long*>(g_hist + 5 * 256 + i), static_cast<unsigned long long>(s));
+    }
+}
+
+// Digit 7 and 6 histograms as the row and column sums of the joint histogram.
+__global__ void __launch_bounds__(256) joint_marginals_kernel(const std::uint64_t* __restrict__ g_joint,
+                                                              std::uint64_t* __restrict__ g_hist) {
+    const int t = threadIdx.x;
+    std::uint64_t row = 0, col = 0;
+    for (int q = 0; q < 256; ++q) {
+        row += g_joint[t * 256 + q];
+        col += g_joint[q * 256 + t];
+    }
+    g_hist[7 * 256 + t] += row;
+    g_hist[6 * 256 + t] += col;
+}
+
+// Exclusive scan of the 65536 joint counts (one CTA): cur16[b] = start of 16-bit bucket b,
+// cur8[d] = start of 8-bit bucket d (= cur16[d << 8]).
+__global__ void __launch_bounds__(1024) joint_scan_kernel(const std::uint64_t* __restrict__ g_joint,
+                                                          std::uint64_t* __restrict__ cur16,
+                                                          std::uint64_t* __restrict__ cur8) {
+    __shared__ std::uint64_t s_w[32];
+    constexpr int PER = JOINT_BINS / 1024;  // 64
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    std::uint64_t sum = 0;
+    for (int q = 0; q < PER; ++q) sum += g_joint[t * PER + q];
+    std::uint64_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    std::uint64_t base = 0;
+    for (int i = 0; i < w; ++i) base += s_w[i];
+    std::uint64_t run = base + inc - sum;
+    for (int q = 0; q < PER; ++q) {
+        const int b = t * PER + q;
+        cur16[b] = run;
+        if ((b & 0xff) == 0) cur8[b >> 8] = run;
+        run += g_joint[b];
+    }
+}
+
+constexpr int MP_BLOCK = 512;
+constexpr int MP_ITEMS = 16;
+constexpr int MP_TILE = MP_BLOCK * MP_ITEMS;  // 8192 keys
+constexpr int MP_SPAN = 4;                    // LEVEL 2: top buckets a tile may span on chip
+constexpr int MP_BINS = 256 * MP_SPAN;
+
+struct mp_smem {
+    static constexpr std::size_t stage_off = 0;
+    static constexpr std::size_t stage_bytes = 8 * MP_TILE;
+    static constexpr std::size_t cnt_off = stage_bytes;  // u32 counts, then local starts
+    static constexpr std::size_t gofs_off = cnt_off + 4 * MP_BINS;
+    static constexpr std::size_t wsum_off = gofs_off + 8 * MP_BINS;
+    static constexpr std::size_t misc_off = wsum_off + 4 * (MP_BLOCK / 32);
+    static constexpr std::size_t total = misc_off + 16;
+};
+
+template <typename T, int LEVEL>
+__global__ void __launch_bounds__(MP_BLOCK, 2)
+    msd_pass_kernel(const T* __restrict__ in, T* __restrict__ out, std::uint64_t n, int desc,
+                    std::uint64_t* __restrict__ cursors) {
+    using L = mp_smem;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* s_stage = reinterpret_cast<T*>(smem + L::stage_off);
+    std::uint32_t* s_cnt = reinterpret_cast<std::uint32_t*>(smem + L::cnt_off);
+    std::uint64_t* s_gofs = reinterpret_cast<std::uint64_t*>(smem + L::gofs_off);
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    std::uint32_t* s_misc = reinterpret_cast<std::uint32_t*>(smem + L::misc_off);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool dsc = desc != 0;
+    const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * MP_TILE;
+    const std::uint32_t len = static_cast<std::uint32_t>(n - t0 < MP_TILE ? n - t0 : MP_TILE);
+
+    // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL 2 = 16-bit prefixes of
+    // the (already top-digit partitioned) tile, relative to its first key's top digit
+    std::uint32_t lo16 = 0, span = 1;
+    if (LEVEL == 2) {
+        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> 56);
+        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> 56);
+        lo16 = f << 8;
+        span = l - f + 1;
+    }
+    const std::uint32_t nbins = LEVEL == 1 ? 256u : 256u * span;
+    if (LEVEL == 2 && span > MP_SPAN) {
+        // tiny top buckets (skewed keys): per-key cursor claims, written straight out
+        for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
+            const T k = in[t0 + j];
+            const std::uint32_t b16 = static_cast<std::uint32_t>(ord64(k, dsc) >> 48);
+            const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + b16), 1ull);
+            out[p] = k;
+        }
+        return;
+    }
+    for (std::uint32_t i = tid; i < nbins; i += MP_BLOCK) s_cnt[i] = 0;
+
+    // load: 128-bit vectors when the tile is full and aligned
+    T k[MP_ITEMS];
+    const bool vec = len == MP_TILE && (reinterpret_cast<std::uintptr_t>(in + t0) & 15) == 0;
+    if (vec) {
+        const uint4* v = reinterpret_cast<const uint4*>(in + t0);
+#pragma unroll
+        for (int i = 0; i < MP_ITEMS / 2; ++i) {
+            const uint4 a = __ldg(v + i * MP_BLOCK + tid);
+            k[2 * i] = reinterpret_cast<const T*>(&a)[0];
+            k[2 * i + 1] = reinterpret_cast<const T*>(&a)[1];
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < MP_ITEMS / 2; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const std::uint32_t li = 2 * (i * MP_BLOCK + tid) + h;
+                k[2 * i + h] = li < len ? in[t0 + li] : T(0);
+            }
+    }
+    auto item_ok = [&](int i) { return 2 * ((i / 2) * MP_BLOCK + tid) + (i & 1) < static_cast<int>(len); };
+    auto bin_of = [&](T key) {
+        const std::uint64_t o = ord64(key, dsc);
+        return LEVEL == 1 ? static_cast<std::uint32_t>(o >> 56) : static_cast<std::uint32_t>(o >> 48) - lo16;
+    };
+    __syncthreads();
+    // slots inside the bins (arbitrary order): one shared atomic per key
+    std::uint32_t sl[MP_ITEMS / 2];
+#pragma unroll
+    for (int i = 0; i < MP_ITEMS / 2; ++i) sl[i] = 0;
+#pragma unroll
+    for (int i = 0; i < MP_ITEMS; ++i)
+        if (item_ok(i)) sl[i / 2] |= atomicAdd(&s_cnt[bin_of(k[i])], 1u) << (16 * (i & 1));
+    __syncthreads();
+    // bin starts (exclusive scan over <= 1024 bins, 2 per thread) + global claims
+    {
+        const std::uint32_t b0 = 2 * tid, b1 = 2 * tid + 1;
+        const std::uint32_t c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
+        const std::uint32_t sum = c0 + c1;
+        std::uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(FULLM, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        std::uint32_t wp = 0;
+#pragma unroll
+        for (int w = 0; w < MP_BLOCK / 32; ++w) wp += w < warp ? s_wsum[w] : 0u;
+        const std::uint32_t st0 = wp + inc - sum, st1 = st0 + c0;
+        // global position of staged slot j in bin b = gofs[b] + j
+        if (c0) {
+            const std::uint64_t g = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + b0),
+                                              static_cast<unsigned long long>(c0));
+            s_gofs[b0] = g - st0;
+        }
+        if (c1) {
+            const std::uint64_t g = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + b1),
+                                              static_cast<unsigned long long>(c1));
+            s_gofs[b1] = g - st1;
+        }
+        __syncthreads();  // every count read before the starts overwrite them
+        if (b0 < nbins) s_cnt[b0] = st0;
+        if (b1 < nbins) s_cnt[b1] = st1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MP_ITEMS; ++i)
+        if (item_ok(i)) s_stage[s_cnt[bin_of(k[i])] + ((sl[i / 2] >> (16 * (i & 1))) & 0xffffu)] = k[i];
+    __syncthreads();
+    // contiguous per-bin runs: consecutive staged slots of one bin go to consecutive addresses
+#pragma unroll 4
+    for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
+        const T key = s_stage[j];
+        out[s_gofs[bin_of(key)] + j] = key;
+    }
+    (void)s_misc;
+}
+
+}  // namespace
+
+template <typename T>
+void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint) {
+    static bool configured = false;
+    constexpr std::size_t smem = JOINT_BINS * 2 + 256 * JH_PARTS * 4;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(hist_joint_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        configured = true;
+    }
+    AKB_CUDA(cudaMemsetAsync(g_joint, 0, JOINT_BINS * sizeof(std::uint64_t), c->stream));
+    const int tok = ctx_prof_begin(c, KF_HIST);
+    hist_joint_kernel<T><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    joint_marginals_kernel<<<1, 256, 0, c->stream>>>(g_joint, g_hist);
+    AKB_CUDA(cudaGetLastError());
+    c->kernel_launches += 2;
+}
+
+template <typename T>
+void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool desc, const std::uint64_t* g_joint,
+               std::uint64_t* cur16, std::uint64_t* cur8) {
+    static bool configured = false;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(msd_pass_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(mp_smem::total)));
+        AKB_CUDA(cudaFuncSetAttribute(msd_pass_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(mp_smem::total)));
+        configured = true;
+    }
+    joint_scan_kernel<<<1, 1024, 0, c->stream>>>(g_joint, cur16, cur8);
+    AKB_CUDA(cudaGetLastError());
+    const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
+    int tok = ctx_prof_begin(c, KF_MSD);
+    msd_pass_kernel<T, 1><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kmid, n, desc ? 1 : 0, cur8);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    tok = ctx_prof_begin(c, KF_MSD);
+    msd_pass_kernel<T, 2><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kmid, kout, n, desc ? 1 : 0, cur16);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 3;
+}
+
+template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t, bool, std::uint64_t*,
+                                     std::uint64_t*);
+template void msd_hist<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t, bool, std::uint64_t*,
+                                      std::uint64_t*);
+template void msd_top16<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::int64_t*, std::uint64_t,
+                                      bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*);
+template void msd_top16<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t*, std::uint64_t,
+                                       bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*);
+
+}  // namespace akb

@@ -1,0 +1,22 @@
+// msd_pass.cuh -- unstable MSD top-digit partition passes (keys-only 64-bit integers).
+#pragma once
+
+#include <cstdint>
+
+#include "ak_common.cuh"
+#include "ctx.cuh"
+
+namespace akb {
+
+// One read of the keys: g_hist rows 5..7 (+=, top three 8-bit digits of the ordered key)
+// and g_joint[65536] (= the histogram of the top 16 bits; zeroed here).
+template <typename T>
+void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint);
+
+// Two partition passes (kin -> kmid by the top 8 bits, kmid -> kout by the top 16 bits);
+// afterwards kout is ordered by its top 16 bits (order inside a 16-bit bucket arbitrary).
+template <typename T>
+void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool desc, const std::uint64_t* g_joint,
+               std::uint64_t* cur16, std::uint64_t* cur8);
+
+}  // namespace akb

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "radix_sort.cuh"
+#include "msd_pass.cuh"
 
 namespace akb {
 
@@ -1403,6 +1404,14 @@ __global__ void bucket_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, 
     cuts[j] = lo;
 }
 
+int msd_env() {
+    static const int v = [] {
+        const char* e = std::getenv("AKB_MSD");  // "0": stable onesweep top-digit passes
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 int hybrid_env() {
     static const int v = [] {
         const char* e = std::getenv("AKB_HYBRID");  // "0" disables (plain LSD), "m" forces m top passes
@@ -1500,7 +1509,18 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         const int blocks = c->sm_count * 4;
         AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
         int first = PASSES - 3;
+        // 64-bit integer keys: the first read also builds the 16-bit joint histogram that
+        // the unstable MSD passes start their cursors from
+        const bool msd_ok = msd_env() != 0 && std::is_integral_v<T> && sizeof(T) == 8 && env <= 0 &&
+                            n >= (std::uint64_t(1) << 24);  // below: the joint-histogram flush dominates
+        std::uint64_t* msdbuf = msd_ok ? ctx_msd(c) : nullptr;
+        bool joint_valid = false;
         auto run_hist = [&](int f) {
+            if (f == PASSES - 3 && msd_ok) {
+                msd_hist<T>(c, kin, n, desc, g_hist, msdbuf);
+                joint_valid = true;
+                return;
+            }
             const int tok = ctx_prof_begin(c, KF_HIST);
             if (f == PASSES - 3) hist_kernel<T, PASSES, PASSES - 3><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
             else hist_kernel<T, PASSES, 0><<<blocks, 256, 0, c->stream>>>(kin, n, desc, g_hist);
@@ -1576,12 +1596,19 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         AKB_CUDA(cudaGetLastError());
         c->kernel_launches += 1;
         const T* cur = kin;
-        for (int q = 0; q < m; ++q) {
-            const int p = top - m + q;
-            T* dst = (q % 2 == 0) ? kalt : kout;
-            launch_pass<T, std::uint32_t, SORT_KEYS>(c, cur, dst, nullptr, nullptr, n, 8 * p, desc, p,
-                                                     g_offs + p * RADIX, counters + p, true);
-            cur = dst;
+        if (joint_valid && m == 2 && top == PASSES) {
+            // unstable MSD partition by the top 16 bits (keys-only integers: order among
+            // equal keys is unobservable)
+            msd_top16<T>(c, kin, kalt, kout, n, desc, msdbuf, msdbuf + 65536, msdbuf + 2 * 65536);
+            cur = kout;
+        } else {
+            for (int q = 0; q < m; ++q) {
+                const int p = top - m + q;
+                T* dst = (q % 2 == 0) ? kalt : kout;
+                launch_pass<T, std::uint32_t, SORT_KEYS>(c, cur, dst, nullptr, nullptr, n, 8 * p, desc, p,
+                                                         g_offs + p * RADIX, counters + p, true);
+                cur = dst;
+            }
         }
         G = cur;
     }

@@ -17,7 +17,7 @@ for r in range(3):
 ex.set_profiling(False)
 tot = 0
 out = []
-for f in ("hist", "onesweep", "local", "other"):
+for f in ("hist", "msd", "onesweep", "local", "other"):
     ms, cnt = ex.kernel_time(f)
     tot += ms
     out.append(f"{f}={ms:.3f}ms/{cnt}")
