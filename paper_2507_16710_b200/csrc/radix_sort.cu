@@ -1584,7 +1584,11 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                 bucket_mode = true;
                 items = ib;
             } else {
-                step = static_cast<std::uint64_t>(LOCAL_TILE - need);
+                // ranges of several buckets: cap them at 12-item CTAs (4608 keys), whose
+                // counting kernel keeps two CTAs per SM (16-item ones fit only one)
+                const bool counting = std::is_integral_v<T> && local_count_env() != 0 && need <= LOCAL_BLOCK * 6;
+                if (counting) items = 12;
+                step = static_cast<std::uint64_t>((counting ? LOCAL_BLOCK * 12 : LOCAL_TILE) - need);
                 if (step < 256) step = 256;
             }
             break;
