@@ -17,6 +17,7 @@
 // After the two passes the array is ordered by its top 16 bits, exactly as the stable
 // top-digit onesweep passes leave it up to the order inside each 16-bit bucket, which the
 // local stage sorts anyway.
+#include <algorithm>
 #include <cstdint>
 
 #include "msd_pass.cuh"
@@ -107,45 +108,53 @@ __global__ void __launch_bounds__(JH_BLOCK, 1)
     }
 }
 
-// Digit 7 and 6 histograms as the row and column sums of the joint histogram.
-__global__ void __launch_bounds__(256) joint_marginals_kernel(const std::uint64_t* __restrict__ g_joint,
-                                                              std::uint64_t* __restrict__ g_hist) {
-    const int t = threadIdx.x;
-    std::uint64_t row = 0, col = 0;
-    for (int q = 0; q < 256; ++q) {
-        row += g_joint[t * 256 + q];
-        col += g_joint[q * 256 + t];
-    }
-    g_hist[7 * 256 + t] += row;
-    g_hist[6 * 256 + t] += col;
-}
-
-// Exclusive scan of the 65536 joint counts (one CTA): cur16[b] = start of 16-bit bucket b,
-// cur8[d] = start of 8-bit bucket d (= cur16[d << 8]).
+// Exclusive scan of the 65536 joint counts (one CTA, warp w owns [2048 w, 2048 w + 2048),
+// coalesced): cur16[b] = start of 16-bit bucket b, cur8[d] = start of 8-bit bucket d; and
+// the digit-7 / digit-6 histograms (rows 7, 6 of g_hist) as the joint's row / column sums.
 __global__ void __launch_bounds__(1024) joint_scan_kernel(const std::uint64_t* __restrict__ g_joint,
                                                           std::uint64_t* __restrict__ cur16,
-                                                          std::uint64_t* __restrict__ cur8) {
+                                                          std::uint64_t* __restrict__ cur8,
+                                                          std::uint64_t* __restrict__ g_hist) {
     __shared__ std::uint64_t s_w[32];
-    constexpr int PER = JOINT_BINS / 1024;  // 64
+    __shared__ std::uint64_t s_col[4][256];
+    constexpr int PER_WARP = JOINT_BINS / 32;  // 2048 = 8 rows of 256
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const std::uint64_t* src = g_joint + w * PER_WARP;
     std::uint64_t sum = 0;
-    for (int q = 0; q < PER; ++q) sum += g_joint[t * PER + q];
-    std::uint64_t inc = sum;
+    for (int c = 0; c < PER_WARP / 32; ++c) sum += src[c * 32 + lane];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
-        if (lane >= o) inc += y;
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULLM, sum, o);
+    if (lane == 0) s_w[w] = sum;
+    // column sums: thread t adds column t & 255 over rows (t >> 8) * 64 .. + 63
+    {
+        const int col = t & 255, r0 = (t >> 8) * 64;
+        std::uint64_t cs = 0;
+        for (int r = r0; r < r0 + 64; ++r) cs += g_joint[r * 256 + col];
+        s_col[t >> 8][col] = cs;
     }
-    if (lane == 31) s_w[w] = inc;
     __syncthreads();
-    std::uint64_t base = 0;
-    for (int i = 0; i < w; ++i) base += s_w[i];
-    std::uint64_t run = base + inc - sum;
-    for (int q = 0; q < PER; ++q) {
-        const int b = t * PER + q;
-        cur16[b] = run;
-        if ((b & 0xff) == 0) cur8[b >> 8] = run;
-        run += g_joint[b];
+    if (t < 256) g_hist[6 * 256 + t] += s_col[0][t] + s_col[1][t] + s_col[2][t] + s_col[3][t];
+    std::uint64_t carry = 0;
+    for (int i = 0; i < w; ++i) carry += s_w[i];
+    std::uint64_t row = 0;
+    for (int c = 0; c < PER_WARP / 32; ++c) {
+        const int b = w * PER_WARP + c * 32 + lane;
+        const std::uint64_t v = g_joint[b];
+        std::uint64_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
+            if (lane >= o) inc += y;
+        }
+        cur16[b] = carry + inc - v;
+        if ((b & 0xff) == 0) cur8[b >> 8] = carry + inc - v;
+        const std::uint64_t tot = __shfl_sync(FULLM, inc, 31);
+        carry += tot;
+        row += tot;
+        if ((c & 7) == 7) {  // a 256-bin row (8 chunks) is complete: digit-7 histogram
+            if (lane == 0) g_hist[7 * 256 + (b >> 8)] += row;
+            row = 0;
+        }
     }
 }
 
@@ -299,9 +308,9 @@ void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t
     hist_joint_kernel<T><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
-    joint_marginals_kernel<<<1, 256, 0, c->stream>>>(g_joint, g_hist);
+    joint_scan_kernel<<<1, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, g_joint + 2 * JOINT_BINS, g_hist);
     AKB_CUDA(cudaGetLastError());
-    c->kernel_launches += 2;
+    c->kernel_launches += 1;
 }
 
 template <typename T>
@@ -315,8 +324,6 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
                                       static_cast<int>(mp_smem::total)));
         configured = true;
     }
-    joint_scan_kernel<<<1, 1024, 0, c->stream>>>(g_joint, cur16, cur8);
-    AKB_CUDA(cudaGetLastError());
     const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
     int tok = ctx_prof_begin(c, KF_MSD);
     msd_pass_kernel<T, 1><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kmid, n, desc ? 1 : 0, cur8);
@@ -326,7 +333,7 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
     msd_pass_kernel<T, 2><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kmid, kout, n, desc ? 1 : 0, cur16);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
-    c->kernel_launches += 3;
+    c->kernel_launches += 2;
 }
 
 template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t, bool, std::uint64_t*,

@@ -8,8 +8,9 @@
 
 namespace akb {
 
-// One read of the keys: g_hist rows 5..7 (+=, top three 8-bit digits of the ordered key)
-// and g_joint[65536] (= the histogram of the top 16 bits; zeroed here).
+// One read of the keys: g_hist rows 5..7 (+=, top three 8-bit digits of the ordered key),
+// g_joint[0 .. 65536) = the histogram of the top 16 bits, and its exclusive scans:
+// g_joint[65536 + b] = start of 16-bit bucket b, g_joint[131072 + d] = start of 8-bit bucket d.
 template <typename T>
 void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint);
 

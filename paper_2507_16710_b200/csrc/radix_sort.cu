@@ -1600,7 +1600,9 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         AKB_CUDA(cudaGetLastError());
         c->kernel_launches += 1;
         const T* cur = kin;
-        if (joint_valid && m == 2 && top == PASSES) {
+        const bool tma_ok = (reinterpret_cast<std::uintptr_t>(kin) & 15) == 0 &&
+                            (reinterpret_cast<std::uintptr_t>(kalt) & 15) == 0;  // TMA-fed passes
+        if (joint_valid && m == 2 && top == PASSES && tma_ok) {
             // unstable MSD partition by the top 16 bits (keys-only integers: order among
             // equal keys is unobservable)
             msd_top16<T>(c, kin, kalt, kout, n, desc, msdbuf, msdbuf + 65536, msdbuf + 2 * 65536);
