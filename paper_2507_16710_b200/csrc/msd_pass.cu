@@ -158,8 +158,17 @@ __global__ void __launch_bounds__(1024) joint_scan_kernel(const std::uint64_t* _
     }
 }
 
-constexpr int MP_BLOCK = 512;
-constexpr int MP_ITEMS = 16;
+#ifndef AKB_MP_BLOCK
+#define AKB_MP_BLOCK 512
+#endif
+constexpr int MP_BLOCK = AKB_MP_BLOCK;
+#ifndef AKB_MP_ITEMS
+#define AKB_MP_ITEMS 16
+#endif
+#ifndef AKB_MP_MINB
+#define AKB_MP_MINB 2
+#endif
+constexpr int MP_ITEMS = AKB_MP_ITEMS;
 constexpr int MP_TILE = MP_BLOCK * MP_ITEMS;  // 8192 keys
 constexpr int MP_SPAN = 4;                    // LEVEL 2: top buckets a tile may span on chip
 constexpr int MP_BINS = 256 * MP_SPAN;
@@ -175,7 +184,7 @@ struct mp_smem {
 };
 
 template <typename T, int LEVEL>
-__global__ void __launch_bounds__(MP_BLOCK, 2)
+__global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     msd_pass_kernel(const T* __restrict__ in, T* __restrict__ out, std::uint64_t n, int desc,
                     std::uint64_t* __restrict__ cursors) {
     using L = mp_smem;

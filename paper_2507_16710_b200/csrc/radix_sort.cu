@@ -1091,9 +1091,7 @@ struct lc_smem {
     static constexpr std::size_t buf_off = 0;
     static constexpr std::size_t cnt_off = 2 * buf_bytes;
     static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LC_WORDS + 4);
-    static constexpr std::size_t side_off = cnt_off + cnt_bytes;  // u16 per staged key: slot | bin size << 8
-    static constexpr std::size_t side_bytes = (sizeof(std::uint16_t) * CAP + 15) & ~std::size_t(15);
-    static constexpr std::size_t red_off = side_off + side_bytes;  // 2 x WARPS x u64 or/and partials
+    static constexpr std::size_t red_off = cnt_off + cnt_bytes;  // 2 x WARPS x u64 or/and partials
     static constexpr std::size_t wsum_off = red_off + 2 * LC_WARPS * sizeof(std::uint64_t);
     static constexpr std::size_t bar_off = wsum_off + 2 * LC_WARPS * sizeof(std::uint32_t);
     static constexpr std::size_t total = bar_off + 2 * sizeof(std::uint64_t);
@@ -1123,7 +1121,6 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
     extern __shared__ __align__(16) unsigned char smem[];
     std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + L::cnt_off);  // packed u16 counts
     std::uint16_t* s_c16 = reinterpret_cast<std::uint16_t*>(smem + L::cnt_off);
-    std::uint16_t* s_side = reinterpret_cast<std::uint16_t*>(smem + L::side_off);
     B* s_red = reinterpret_cast<B*>(smem + L::red_off);
     std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
     std::uint64_t* s_bar = reinterpret_cast<std::uint64_t*>(smem + L::bar_off);
@@ -1213,11 +1210,17 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
             __syncthreads();  // s_red is rewritten by the next range
             continue;
         }
-        B any1 = 0, all1 = static_cast<B>(~B(0));
+        // lanes 0-15 fold the OR partials, lanes 16-31 the AND partials (one load per lane)
+        B any1, all1;
+        {
+            B x = s_red[lane];
 #pragma unroll
-        for (int w = 0; w < LC_WARPS; ++w) {
-            any1 |= s_red[w];
-            all1 &= s_red[LC_WARPS + w];
+            for (int o = 8; o > 0; o >>= 1) {
+                const B y = __shfl_xor_sync(FULL, x, o);
+                x = lane < 16 ? (x | y) : (x & y);
+            }
+            any1 = __shfl_sync(FULL, x, 0);
+            all1 = __shfl_sync(FULL, x, 16);
         }
         const B vary = any1 & ~all1;
         if (vary == 0) {  // every key equal: the range is already sorted
@@ -1281,9 +1284,9 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
                 const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
                 if (lane == 0) s_wsum[warp] = T0 + T1;
                 __syncthreads();
-                std::uint32_t wp = 0;
+                std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;  // lane-parallel warp prefix
 #pragma unroll
-                for (int w = 0; w < LC_WARPS; ++w) wp += w < warp ? s_wsum[w] : 0u;
+                for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
                 const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
 #pragma unroll
                 for (int q = 0; q < 2; ++q)
@@ -1328,16 +1331,11 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
             if (tid == 0) s_c16[2 * nwords] = static_cast<std::uint16_t>(len);  // end of the last bin
         }
         __syncthreads();
-        // scatter into bin order; side[staged slot] = slot in bin | bin size << 8
+        // scatter into bin order (ordered bits: ranked as unsigned)
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len) {
-                const std::uint32_t bn = pk[i] & 0xffffu, slot = pk[i] >> 16;
-                const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
-                reinterpret_cast<B*>(s_stage)[st + slot] = ordered(k[i], DESC);  // ranked as unsigned bits
-                s_side[st + slot] = static_cast<std::uint16_t>(slot | (cnt << 8));
-            }
-        }
+        for (int i = 0; i < ITEMS; ++i)
+            if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len)
+                reinterpret_cast<B*>(s_stage)[s_c16[pk[i] & 0xffffu] + (pk[i] >> 16)] = ordered(k[i], DESC);
         __syncthreads();
         // each staged position ranks its key inside its (short) bin on the full key:
         // final slot = bin start + #(key, staged slot) lexicographically smaller
@@ -1345,11 +1343,12 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
 #pragma unroll 1
         for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
             const B v = s_ord[x];
-            const std::uint32_t sd = s_side[x];
-            const std::uint32_t cnt = sd >> 8;
+            // bin extent: consecutive positions have nondecreasing bins, so a warp's counter
+            // reads fall in a few words
+            const std::uint32_t bn = static_cast<std::uint32_t>(v >> shift) & bmask;
+            const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
             std::uint32_t rk = x;
             if (cnt > 1) {
-                const std::uint32_t st = x - (sd & 0xffu);
                 rk = st + lex_less96(s_ord[st], st, v, x) + lex_less96(s_ord[st + 1], st + 1, v, x);
 #pragma unroll 1
                 for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(s_ord[y], y, v, x);
@@ -1357,6 +1356,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
             const B o = DESC ? static_cast<B>(~v) : v;
             out[b + rk] = static_cast<T>(std::is_signed_v<T> ? (o ^ (B(1) << (8 * sizeof(B) - 1))) : o);
         }
+        __syncthreads();  // the counters are read above and zeroed by the next range
     }  // ranges
 }
 
