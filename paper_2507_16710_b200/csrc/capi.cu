@@ -457,6 +457,7 @@ int ak_ctx_destroy(ak_ctx* c) {
         if (c->split) cudaFree(c->split);
         if (c->cuts) cudaFree(c->cuts);
         if (c->msd) cudaFree(c->msd);
+        if (c->msd3) cudaFree(c->msd3);
         if (c->stage) cudaFree(c->stage);
         if (c->pinned) cudaFreeHost(c->pinned);
         for (auto& t : c->pending) {

@@ -153,6 +153,12 @@ std::uint64_t* ctx_msd(ak_ctx* c) {
     return c->msd;
 }
 
+std::uint64_t* ctx_msd3(ak_ctx* c) {
+    if (!c->msd3)
+        AKB_CUDA(cudaMalloc(&c->msd3, ((std::size_t(1) << 24) + (std::size_t(1) << 23) + 4096) * sizeof(std::uint64_t)));
+    return c->msd3;
+}
+
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count) {
     if (count > c->split_cap) {
         if (c->split) {

@@ -55,6 +55,8 @@ struct ak_ctx {
 
     // hybrid radix sort, MSD passes: 16-bit joint histogram + 16-bit / 8-bit bucket cursors
     std::uint64_t* msd = nullptr;
+    // third MSD level: [2^24 u64 cursors][2^24 u32 counts][4096 u64 chunk sums]
+    std::uint64_t* msd3 = nullptr;
 
     // device staging for the *_host entry points (end-to-end path)
     void* stage = nullptr;
@@ -105,6 +107,7 @@ std::uint64_t* ctx_split(ak_ctx* c, std::size_t count);
 std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count);
 // MSD-pass tables: [65536 joint counts][65536 16-bit cursors][256 8-bit cursors]
 std::uint64_t* ctx_msd(ak_ctx* c);
+std::uint64_t* ctx_msd3(ak_ctx* c);
 void* ctx_stage(ak_ctx* c, std::size_t bytes);
 
 // Kernel families for ak_ctx_kernel_time (C ABI: AK_KF_*).

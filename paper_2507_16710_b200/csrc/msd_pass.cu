@@ -199,22 +199,24 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * MP_TILE;
     const std::uint32_t len = static_cast<std::uint32_t>(n - t0 < MP_TILE ? n - t0 : MP_TILE);
 
-    // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL 2 = 16-bit prefixes of
-    // the (already top-digit partitioned) tile, relative to its first key's top digit
+    // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL L > 1 = the 8L-bit prefixes
+    // of the (already 8(L-1)-bit partitioned) tile, relative to its first key's 8(L-1)-bit
+    // prefix (cursor index = the 8L-bit prefix)
+    constexpr int TOP = 64 - 8 * LEVEL;  // shift of the 8L-bit prefix
     std::uint32_t lo16 = 0, span = 1;
-    if (LEVEL == 2) {
-        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> 56);
-        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> 56);
+    if (LEVEL >= 2) {
+        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> (TOP + 8));
+        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> (TOP + 8));
         lo16 = f << 8;
         span = l - f + 1;
     }
     const std::uint32_t nbins = LEVEL == 1 ? 256u : 256u * span;
-    if (LEVEL == 2 && span > MP_SPAN) {
-        // tiny top buckets (skewed keys): per-key cursor claims, written straight out
+    if (LEVEL >= 2 && span > MP_SPAN) {
+        // tiny buckets (skewed keys): per-key cursor claims, written straight out
         for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
             const T k = in[t0 + j];
-            const std::uint32_t b16 = static_cast<std::uint32_t>(ord64(k, dsc) >> 48);
-            const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + b16), 1ull);
+            const std::uint32_t bp = static_cast<std::uint32_t>(ord64(k, dsc) >> TOP);
+            const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + bp), 1ull);
             out[p] = k;
         }
         return;
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     auto item_ok = [&](int i) { return 2 * ((i / 2) * MP_BLOCK + tid) + (i & 1) < static_cast<int>(len); };
     auto bin_of = [&](T key) {
         const std::uint64_t o = ord64(key, dsc);
-        return LEVEL == 1 ? static_cast<std::uint32_t>(o >> 56) : static_cast<std::uint32_t>(o >> 48) - lo16;
+        return static_cast<std::uint32_t>(o >> TOP) - lo16;
     };
     __syncthreads();
     // slots inside the bins (arbitrary order): one shared atomic per key
@@ -301,6 +303,117 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     (void)s_misc;
 }
 
+// Third level: histogram of the 24-bit prefixes of a 16-bit-partitioned array. A tile spans
+// few 16-bit buckets (relative bins in shared memory), flushed with one global atomic per
+// non-empty bin into hist24[2^24] (u32 counts; n < 2^32 per sort).
+template <typename T>
+__global__ void __launch_bounds__(MP_BLOCK) hist24_kernel(const T* __restrict__ in, std::uint64_t n, int desc,
+                                                        std::uint32_t* __restrict__ hist24) {
+    __shared__ std::uint32_t s_cnt[MP_BINS];
+    const int tid = threadIdx.x;
+    const bool dsc = desc != 0;
+    const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * MP_TILE;
+    const std::uint32_t len = static_cast<std::uint32_t>(n - t0 < MP_TILE ? n - t0 : MP_TILE);
+    const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> 48);
+    const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> 48);
+    const std::uint32_t lo = f << 8, span = l - f + 1;
+    if (span > MP_SPAN) {
+        for (std::uint32_t j = tid; j < len; j += MP_BLOCK)
+            atomicAdd(hist24 + static_cast<std::uint32_t>(ord64(in[t0 + j], dsc) >> 40), 1u);
+        return;
+    }
+    for (int i = tid; i < MP_BINS; i += MP_BLOCK) s_cnt[i] = 0;
+    __syncthreads();
+    if (len == MP_TILE && (reinterpret_cast<std::uintptr_t>(in + t0) & 15) == 0) {
+        const uint4* v = reinterpret_cast<const uint4*>(in + t0);
+#pragma unroll 4
+        for (int i = tid; i < MP_TILE / 2; i += MP_BLOCK) {
+            const uint4 a = __ldg(v + i);
+            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(reinterpret_cast<const T*>(&a)[0], dsc) >> 40) - lo], 1u);
+            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(reinterpret_cast<const T*>(&a)[1], dsc) >> 40) - lo], 1u);
+        }
+    } else {
+        for (std::uint32_t j = tid; j < len; j += MP_BLOCK)
+            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(in[t0 + j], dsc) >> 40) - lo], 1u);
+    }
+    __syncthreads();
+    for (std::uint32_t i = tid; i < 256 * span; i += MP_BLOCK)
+        if (s_cnt[i]) atomicAdd(hist24 + lo + i, s_cnt[i]);
+}
+
+// Exclusive scan of hist24 (2^24 u32) into cur24 (u64), three launches: chunk sums,
+// one-CTA scan of the 4096 chunk sums, chunk-local scans.
+constexpr int S24_CHUNK = 4096;
+__global__ void __launch_bounds__(1024) scan24_sums_kernel(const std::uint32_t* __restrict__ h,
+                                                           std::uint64_t* __restrict__ sums) {
+    __shared__ std::uint64_t s_w[32];
+    const int t = threadIdx.x;
+    const uint4 v = reinterpret_cast<const uint4*>(h + static_cast<std::size_t>(blockIdx.x) * S24_CHUNK)[t];
+    std::uint64_t x = static_cast<std::uint64_t>(v.x) + v.y + v.z + v.w;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLM, x, o);
+    if ((t & 31) == 0) s_w[t >> 5] = x;
+    __syncthreads();
+    if (t < 32) {
+        std::uint64_t y = s_w[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(FULLM, y, o);
+        if (t == 0) sums[blockIdx.x] = y;
+    }
+}
+__global__ void __launch_bounds__(1024) scan24_top_kernel(std::uint64_t* __restrict__ sums, int nchunks) {
+    __shared__ std::uint64_t s_w[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    constexpr int PER = 4;  // 4096 chunks max
+    std::uint64_t v[PER], tot = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        v[q] = t * PER + q < nchunks ? sums[t * PER + q] : 0;
+        tot += v[q];
+    }
+    std::uint64_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    std::uint64_t base = 0;
+    for (int i = 0; i < w; ++i) base += s_w[i];
+    std::uint64_t run = base + inc - tot;
+#pragma unroll
+    for (int q = 0; q < PER; ++q)
+        if (t * PER + q < nchunks) {
+            sums[t * PER + q] = run;
+            run += v[q];
+        }
+}
+__global__ void __launch_bounds__(1024) scan24_chunk_kernel(const std::uint32_t* __restrict__ h,
+                                                            const std::uint64_t* __restrict__ sums,
+                                                            std::uint64_t* __restrict__ cur) {
+    __shared__ std::uint64_t s_w[32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const std::size_t base = static_cast<std::size_t>(blockIdx.x) * S24_CHUNK;
+    const uint4 v = reinterpret_cast<const uint4*>(h + base)[t];
+    const std::uint64_t tot = static_cast<std::uint64_t>(v.x) + v.y + v.z + v.w;
+    std::uint64_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    std::uint64_t run = sums[blockIdx.x] + inc - tot;
+    for (int i = 0; i < w; ++i) run += s_w[i];
+    std::uint64_t* o = cur + base + 4 * t;
+    o[0] = run;
+    o[1] = run + v.x;
+    o[2] = run + v.x + v.y;
+    o[3] = run + v.x + v.y + v.z;
+}
+
 }  // namespace
 
 template <typename T>
@@ -345,6 +458,37 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
     c->kernel_launches += 2;
 }
 
+template <typename T>
+void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc) {
+    static bool configured = false;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(msd_pass_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(mp_smem::total)));
+        configured = true;
+    }
+    std::uint64_t* cur24 = ctx_msd3(c);                                   // 2^24 u64 cursors
+    std::uint32_t* hist24 = reinterpret_cast<std::uint32_t*>(cur24 + (1u << 24));  // 2^24 u32 counts
+    std::uint64_t* sums = cur24 + (1u << 24) + (1u << 23);               // 4096 chunk sums
+    AKB_CUDA(cudaMemsetAsync(hist24, 0, (std::size_t(1) << 24) * sizeof(std::uint32_t), c->stream));
+    const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
+    int tok = ctx_prof_begin(c, KF_HIST);
+    hist24_kernel<T><<<tiles, MP_BLOCK, 0, c->stream>>>(kin, n, desc ? 1 : 0, hist24);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    constexpr int nchunks = (1 << 24) / S24_CHUNK;
+    scan24_sums_kernel<<<nchunks, 1024, 0, c->stream>>>(hist24, sums);
+    scan24_top_kernel<<<1, 1024, 0, c->stream>>>(sums, nchunks);
+    scan24_chunk_kernel<<<nchunks, 1024, 0, c->stream>>>(hist24, sums, cur24);
+    AKB_CUDA(cudaGetLastError());
+    tok = ctx_prof_begin(c, KF_MSD);
+    msd_pass_kernel<T, 3><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kout, n, desc ? 1 : 0, cur24);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 5;
+}
+
+template void msd_level3<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::uint64_t, bool);
+template void msd_level3<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t, bool);
 template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t, bool, std::uint64_t*,
                                      std::uint64_t*);
 template void msd_hist<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t, bool, std::uint64_t*,

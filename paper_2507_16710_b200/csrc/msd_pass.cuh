@@ -20,4 +20,10 @@ template <typename T>
 void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool desc, const std::uint64_t* g_joint,
                std::uint64_t* cur16, std::uint64_t* cur8);
 
+// Third partition level (n >= 2^29): kin (ordered by its top 16 bits) -> kout ordered by
+// its top 24 bits; the 24-bit histogram is built by an extra read of kin (tiles span few
+// 16-bit buckets, so it is counted in shared memory), then scanned into 2^24 cursors.
+template <typename T>
+void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc);
+
 }  // namespace akb

@@ -1602,11 +1602,15 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         const T* cur = kin;
         const bool tma_ok = (reinterpret_cast<std::uintptr_t>(kin) & 15) == 0 &&
                             (reinterpret_cast<std::uintptr_t>(kalt) & 15) == 0;  // TMA-fed passes
-        if (joint_valid && m == 2 && top == PASSES && tma_ok) {
-            // unstable MSD partition by the top 16 bits (keys-only integers: order among
+        if (joint_valid && (m == 2 || m == 3) && top == PASSES && tma_ok && n < (std::uint64_t(1) << 32)) {
+            // unstable MSD partition by the top 16 (24) bits (keys-only integers: order among
             // equal keys is unobservable)
             msd_top16<T>(c, kin, kalt, kout, n, desc, msdbuf, msdbuf + 65536, msdbuf + 2 * 65536);
             cur = kout;
+            if (m == 3) {
+                msd_level3<T>(c, kout, kalt, n, desc);
+                cur = kalt;
+            }
         } else {
             for (int q = 0; q < m; ++q) {
                 const int p = top - m + q;
