@@ -13,6 +13,7 @@
 #include "../../include/ak_cuda.h"
 #include "ctx.cuh"
 #include "radix_sort.cuh"
+#include "sortperm_fast.cuh"
 #include "predicates.cuh"
 #include "reduce_scan.cuh"
 #include "search_merge.cuh"
@@ -155,8 +156,16 @@ void sortperm_impl(ak_ctx* c, const T* data, std::uint64_t n, I* out, std::uint6
     if (n == 1) {
         AKB_CUDA(cudaMemsetAsync(out, 0, sizeof(I), c->stream));
     } else if (n > 1) {
-        akb::radix_sort<T, V>(c, akb::SORT_IOTA, data, sk, wk, nullptr, reinterpret_cast<V*>(out),
-                              reinterpret_cast<V*>(si), n, desc != 0, false);
+        bool done = false;
+        // 32-bit integer keys: composite (key, index) keys through the 64-bit hybrid sort
+        // (1e8 i32: 2.31 ms vs 2.64 ms onesweep). Float keys keep the onesweep: their
+        // exponent-heavy top bits need a third MSD level, which costs more than it saves
+        // (1e8 f32 uniform in [-1e6, 1e6): 3.03 ms vs 2.64 ms, measured r01).
+        if constexpr (sizeof(T) == 4 && std::is_integral_v<T>)
+            done = akb::sortperm_composite<T, V>(c, data, n, reinterpret_cast<V*>(out), desc != 0);
+        if (!done)
+            akb::radix_sort<T, V>(c, akb::SORT_IOTA, data, sk, wk, nullptr, reinterpret_cast<V*>(out),
+                                  reinterpret_cast<V*>(si), n, desc != 0, false);
     }
     akb::ctx_finish(c);
 }
@@ -459,6 +468,7 @@ int ak_ctx_destroy(ak_ctx* c) {
         if (c->msd) cudaFree(c->msd);
         if (c->msd3) cudaFree(c->msd3);
         if (c->stage) cudaFree(c->stage);
+        if (c->work) cudaFree(c->work);
         if (c->pinned) cudaFreeHost(c->pinned);
         for (auto& t : c->pending) {
             cudaEventDestroy(t.a);

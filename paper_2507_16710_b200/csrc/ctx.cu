@@ -135,6 +135,24 @@ void* ctx_stage(ak_ctx* c, std::size_t bytes) {
     return c->stage;
 }
 
+void* ctx_work(ak_ctx* c, std::size_t bytes) {
+    if (bytes > c->work_bytes) {
+        if (c->work) {
+            AKB_CUDA(cudaStreamSynchronize(c->stream));
+            AKB_CUDA(cudaFree(c->work));
+            c->work = nullptr;
+            c->work_bytes = 0;
+        }
+        if (cudaMalloc(&c->work, bytes) != cudaSuccess) {
+            cudaGetLastError();  // clear: the caller falls back to the caller-scratch path
+            c->work = nullptr;
+            return nullptr;
+        }
+        c->work_bytes = bytes;
+    }
+    return c->work;
+}
+
 std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count) {
     if (count > c->cuts_cap) {
         if (c->cuts) {
@@ -149,7 +167,7 @@ std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count) {
 }
 
 std::uint64_t* ctx_msd(ak_ctx* c) {
-    if (!c->msd) AKB_CUDA(cudaMalloc(&c->msd, (2 * 65536 + 256) * sizeof(std::uint64_t)));
+    if (!c->msd) AKB_CUDA(cudaMalloc(&c->msd, (2 * 65536 + 256 + 8) * sizeof(std::uint64_t)));
     return c->msd;
 }
 

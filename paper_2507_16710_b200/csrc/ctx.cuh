@@ -58,6 +58,10 @@ struct ak_ctx {
     // third MSD level: [2^24 u64 cursors][2^24 u32 counts][4096 u64 chunk sums]
     std::uint64_t* msd3 = nullptr;
 
+    // work arena of the composite-key sortperm path (two 8-byte words per element)
+    void* work = nullptr;
+    std::size_t work_bytes = 0;
+
     // device staging for the *_host entry points (end-to-end path)
     void* stage = nullptr;
     std::size_t stage_bytes = 0;
@@ -105,10 +109,12 @@ void ctx_finish(ak_ctx* c);  // synchronise when blocking
 void* ctx_pinned(ak_ctx* c, std::size_t bytes);
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count);
 std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count);
-// MSD-pass tables: [65536 joint counts][65536 16-bit cursors][256 8-bit cursors]
+// MSD-pass tables: [65536 joint counts][65536 16-bit cursors][256 8-bit cursors][8 spare]
 std::uint64_t* ctx_msd(ak_ctx* c);
 std::uint64_t* ctx_msd3(ak_ctx* c);
 void* ctx_stage(ak_ctx* c, std::size_t bytes);
+// ctx-owned work arena (grown on demand, reused); nullptr when the allocation fails
+void* ctx_work(ak_ctx* c, std::size_t bytes);
 
 // Kernel families for ak_ctx_kernel_time (C ABI: AK_KF_*).
 enum kernel_family : int { KF_ONESWEEP = 0, KF_HIST = 1, KF_MERGE = 2, KF_REDUCE = 3, KF_SCAN = 4,

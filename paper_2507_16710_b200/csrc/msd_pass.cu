@@ -487,6 +487,39 @@ void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc) {
     c->kernel_launches += 5;
 }
 
+template <typename C>
+__global__ void bucket_max_kernel(const C* __restrict__ h, std::uint64_t cnt, unsigned long long* __restrict__ out) {
+    std::uint64_t m = 0;
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt; i += stride)
+        m = m > h[i] ? m : static_cast<std::uint64_t>(h[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const std::uint64_t y = __shfl_xor_sync(FULLM, m, o);
+        m = m > y ? m : y;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, static_cast<unsigned long long>(m));
+}
+
+std::uint64_t msd_max_bucket(ak_ctx* c, int level) {
+    std::uint64_t* slot = ctx_msd(c) + 2 * JOINT_BINS + 256;
+    AKB_CUDA(cudaMemsetAsync(slot, 0, sizeof(std::uint64_t), c->stream));
+    if (level == 3) {
+        const std::uint32_t* hist24 = reinterpret_cast<const std::uint32_t*>(ctx_msd3(c) + (1u << 24));
+        bucket_max_kernel<std::uint32_t><<<c->sm_count * 4, 256, 0, c->stream>>>(
+            hist24, std::uint64_t(1) << 24, reinterpret_cast<unsigned long long*>(slot));
+    } else {
+        bucket_max_kernel<std::uint64_t><<<64, 256, 0, c->stream>>>(ctx_msd(c), JOINT_BINS,
+                                                                    reinterpret_cast<unsigned long long*>(slot));
+    }
+    AKB_CUDA(cudaGetLastError());
+    auto* h = static_cast<std::uint64_t*>(ctx_pinned(c, sizeof(std::uint64_t)));
+    AKB_CUDA(cudaMemcpyAsync(h, slot, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));
+    c->kernel_launches += 1;
+    return *h;
+}
+
 template void msd_level3<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::uint64_t, bool);
 template void msd_level3<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t, bool);
 template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t, bool, std::uint64_t*,

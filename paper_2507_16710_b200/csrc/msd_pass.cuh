@@ -26,4 +26,7 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
 template <typename T>
 void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc);
 
+// Largest bucket after the MSD levels (level 2: 16-bit buckets, 3: 24-bit), on the host.
+std::uint64_t msd_max_bucket(ak_ctx* c, int level);
+
 }  // namespace akb

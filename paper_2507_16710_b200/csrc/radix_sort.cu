@@ -1611,6 +1611,17 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                 msd_level3<T>(c, kout, kalt, n, desc);
                 cur = kalt;
             }
+            if (!bucket_mode) {
+                // ranges of several buckets: size them from the exact largest bucket (the
+                // plan's estimate assumes independent digits, which skewed keys -- e.g. the
+                // exponent-heavy top bits of composite float keys -- violate)
+                const std::uint64_t maxb = msd_max_bucket(c, m);
+                const std::uint64_t cap = static_cast<std::uint64_t>(LOCAL_BLOCK) * items;
+                if (maxb + 256 <= cap) {
+                    step = cap - maxb;
+                    J = ceil_div(n, step);
+                }
+            }
         } else {
             for (int q = 0; q < m; ++q) {
                 const int p = top - m + q;

@@ -1,0 +1,71 @@
+// sortperm_fast.cu -- sortperm of 32-bit keys through the keys-only 64-bit sort.
+//
+// Composite key = ordered(key) << 32 | index: all composites are distinct, so ANY correct
+// sort of them is unique, and its order is (key, index) lexicographic -- exactly the stable
+// sortperm (equal keys keep ascending index; -0.0 and +0.0 share one ordered value, so they
+// tie and keep input order as under std::less<float>). The composites are sorted by the
+// hybrid 64-bit integer path (unstable MSD partition passes + counting local stage), which
+// runs at ~0.5 of HBM, against ~0.37 for the 4-pass stable onesweep over (key, index) pairs.
+#include <cstdlib>
+
+#include "radix_sort.cuh"
+#include "sortperm_fast.cuh"
+
+namespace akb {
+
+namespace {
+
+template <typename T>
+__global__ void compose_kernel(const T* __restrict__ keys, std::uint64_t n, int desc, std::uint64_t* __restrict__ comp) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        comp[i] = (static_cast<std::uint64_t>(ordered(keys[i], desc != 0)) << 32) | i;
+}
+
+template <typename I>
+__global__ void decompose_kernel(const std::uint64_t* __restrict__ comp, std::uint64_t n, I* __restrict__ out) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = static_cast<I>(comp[i] & 0xffffffffull);
+}
+
+int fast_env() {
+    static const int v = [] {
+        const char* e = std::getenv("AKB_SORTPERM_COMPOSITE");  // "0": stable onesweep over pairs
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+}  // namespace
+
+template <typename T, typename I>
+bool sortperm_composite(ak_ctx* c, const T* data, std::uint64_t n, I* out, bool desc) {
+    static_assert(sizeof(T) == 4, "32-bit keys");
+    if (!fast_env() || n < (std::uint64_t(1) << 20) || n >= (std::uint64_t(1) << 32)) return false;
+    auto* a = static_cast<std::uint64_t*>(ctx_work(c, 2 * n * sizeof(std::uint64_t)));
+    if (!a) return false;
+    std::uint64_t* b = a + n;
+    const unsigned grid = static_cast<unsigned>(c->sm_count * 8);
+    int tok = ctx_prof_begin(c, KF_OTHER);
+    compose_kernel<T><<<grid, 512, 0, c->stream>>>(data, n, desc ? 1 : 0, a);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    radix_sort<std::uint64_t, std::uint32_t>(c, SORT_KEYS, a, a, b, nullptr, nullptr, nullptr, n, false, true);
+    tok = ctx_prof_begin(c, KF_OTHER);
+    decompose_kernel<I><<<grid, 512, 0, c->stream>>>(a, n, out);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 2;
+    return true;
+}
+
+#define AKB_SPC(T, I) template bool sortperm_composite<T, I>(ak_ctx*, const T*, std::uint64_t, I*, bool);
+AKB_SPC(float, std::uint32_t)
+AKB_SPC(float, std::uint64_t)
+AKB_SPC(std::int32_t, std::uint32_t)
+AKB_SPC(std::int32_t, std::uint64_t)
+AKB_SPC(std::uint32_t, std::uint32_t)
+AKB_SPC(std::uint32_t, std::uint64_t)
+
+}  // namespace akb

@@ -161,3 +161,26 @@ def test_config2_sortperm_1e8_f32_properties(ak, ex, dev):
     ak.merge_sort_by_key(k, v, ex=ex)
     assert torch.equal(v.long(), p)
     assert torch.equal(k, s)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.int32, np.uint32])
+@pytest.mark.parametrize("idx", [torch.int32, torch.int64])
+def test_sortperm_composite_path_matches_oracle(ak, orc, ex, dev, dt, idx):
+    """n >= 2^20 32-bit integer keys take the composite (key, index) 64-bit sort
+    (sortperm_fast.cu); float keys the onesweep. Bit-exact vs the oracle, ties and
+    -0.0/+0.0 included, both directions."""
+    n = 1_500_001
+    rng = np.random.default_rng(20)
+    if dt == np.float32:
+        x = rng.uniform(-1e6, 1e6, n).astype(np.float32)
+        x[rng.integers(0, n, 20_000)] = 0.0
+        x[rng.integers(0, n, 20_000)] = -0.0
+        x[rng.integers(0, n, 50_000)] = x[7]
+    else:
+        info = np.iinfo(dt)
+        x = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+        x[rng.integers(0, n, 100_000)] = x[3]
+    for desc in (False, True):
+        want = orc.sortperm(x, descending=desc)
+        p = ak.sortperm(tdev(x, dev), ex=ex, cmp="greater" if desc else None, index_dtype=idx)
+        assert np.array_equal(p.cpu().numpy().astype(np.uint64), want)
