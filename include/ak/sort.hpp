@@ -64,7 +64,8 @@ namespace detail {
 template <typename T>
 inline constexpr bool is_key_v =
     std::is_same_v<T, std::int32_t> || std::is_same_v<T, std::uint32_t> || std::is_same_v<T, std::int64_t> ||
-    std::is_same_v<T, std::uint64_t> || std::is_same_v<T, float> || std::is_same_v<T, double>;
+    std::is_same_v<T, std::uint64_t> || std::is_same_v<T, float> || std::is_same_v<T, double> ||
+    std::is_same_v<T, std::int16_t> || std::is_same_v<T, __int128>;  // dtype.hpp:14-21
 
 template <typename T, typename Cmp>
 constexpr int desc_of() {
@@ -115,11 +116,14 @@ AK_SORT_DISPATCH(i64, std::int64_t)
 AK_SORT_DISPATCH(u64, std::uint64_t)
 AK_SORT_DISPATCH(f32, float)
 AK_SORT_DISPATCH(f64, double)
+AK_SORT_DISPATCH(i16, std::int16_t)
+AK_SORT_DISPATCH(i128, __int128)
 #undef AK_SORT_DISPATCH
 
 template <typename T>
 void require_key() {
-    static_assert(is_key_v<T>, "ak (B200 build): key type must be int32/uint32/int64/uint64/float/double");
+    static_assert(is_key_v<T>,
+                  "ak (B200 build): key type must be int16/int32/uint32/int64/uint64/int128/float/double");
 }
 template <typename V>
 void require_word() {

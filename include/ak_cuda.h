@@ -151,6 +151,35 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int key_bytes);
                                 T* const* out, const uint64_t* out_cap, uint64_t* out_count,    \
                                 const ak_sih_config* cfg, ak_sih_stats* stats);
 
+/* int16 and int128 keys (dtype.hpp:14-21): the sort family only (merge_sort, by_key,
+ * sortperm, sortperm_lowmem); int16 sorts widened to int32, int128 as a stable LSD over its
+ * two 64-bit halves. Uses a ctx-owned work arena. */
+typedef __int128 ak_int128;
+#define AK_DECL_SORT_ONLY(S, T)                                                                 \
+    int ak_merge_sort_##S(ak_ctx* ctx, T* data, uint64_t n, T* scratch, uint64_t scratch_n,      \
+                          int desc);                                                            \
+    int ak_merge_sort_host_##S(ak_ctx* ctx, T* host_data, uint64_t n, int desc);                \
+    int ak_merge_sort_by_key_##S##_b32(ak_ctx* ctx, T* keys, uint64_t n_keys, void* payload,     \
+                                       uint64_t n_payload, T* scratch_keys, uint64_t sk_n,      \
+                                       void* scratch_payload, uint64_t sp_n, int desc);         \
+    int ak_merge_sort_by_key_##S##_b64(ak_ctx* ctx, T* keys, uint64_t n_keys, void* payload,     \
+                                       uint64_t n_payload, T* scratch_keys, uint64_t sk_n,      \
+                                       void* scratch_payload, uint64_t sp_n, int desc);         \
+    int ak_sortperm_##S##_i32(ak_ctx* ctx, const T* data, uint64_t n, int32_t* out,             \
+                              uint64_t out_n, T* working_keys, uint64_t wk_n, T* scratch_keys,  \
+                              uint64_t sk_n, int32_t* scratch_index, uint64_t si_n, int desc);  \
+    int ak_sortperm_##S##_i64(ak_ctx* ctx, const T* data, uint64_t n, int64_t* out,             \
+                              uint64_t out_n, T* working_keys, uint64_t wk_n, T* scratch_keys,  \
+                              uint64_t sk_n, int64_t* scratch_index, uint64_t si_n, int desc);  \
+    int ak_sortperm_lowmem_##S##_i32(ak_ctx* ctx, const T* data, uint64_t n, int32_t* out,      \
+                                     uint64_t out_n, int32_t* scratch_index, uint64_t si_n,     \
+                                     int desc);                                                 \
+    int ak_sortperm_lowmem_##S##_i64(ak_ctx* ctx, const T* data, uint64_t n, int64_t* out,      \
+                                     uint64_t out_n, int64_t* scratch_index, uint64_t si_n,     \
+                                     int desc);
+AK_DECL_SORT_ONLY(i16, int16_t)
+AK_DECL_SORT_ONLY(i128, ak_int128)
+
 AK_DECL_SORT(i32, int32_t)
 AK_DECL_SORT(u32, uint32_t)
 AK_DECL_SORT(i64, int64_t)

@@ -95,6 +95,9 @@ _lib.ak_sort_ctx_bytes.argtypes = [C.c_uint64, C.c_int]
 
 _SUFFIX = {torch.int32: "i32", torch.uint32: "u32", torch.int64: "i64", torch.uint64: "u64",
            torch.float32: "f32", torch.float64: "f64"}
+# sort family only (dtype.hpp:14-21): int16, and int128 as an (n, 2) int64 tensor (low, high
+# words, little endian -- the memory layout of __int128)
+_SORT_SUFFIX = {**_SUFFIX, torch.int16: "i16"}
 _NP_SUFFIX = {np.dtype(np.int32): "i32", np.dtype(np.uint32): "u32", np.dtype(np.int64): "i64",
               np.dtype(np.uint64): "u64", np.dtype(np.float32): "f32", np.dtype(np.float64): "f64"}
 _CT = {"i32": C.c_int32, "u32": C.c_uint32, "i64": C.c_int64, "u64": C.c_uint64, "f32": C.c_float,
@@ -235,6 +238,16 @@ def _suffix(t: torch.Tensor) -> str:
         raise InvalidArgument(f"unsupported dtype {t.dtype}") from None
 
 
+def _sort_keys(t: torch.Tensor) -> tuple[str, int]:
+    """(suffix, element count) of a sort-family key tensor; (n, 2) int64 = n int128 keys."""
+    if t.dtype == torch.int64 and t.dim() == 2 and t.shape[1] == 2:
+        return "i128", t.shape[0]
+    try:
+        return _SORT_SUFFIX[t.dtype], t.numel()
+    except KeyError:
+        raise InvalidArgument(f"unsupported dtype {t.dtype}") from None
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -320,9 +333,9 @@ def merge_sort(data: torch.Tensor, scratch=None, ex: ExecBackend | None = None, 
         scratch = scratch.scratch_keys
     if scratch is None:
         scratch = torch.empty_like(data)
-    s = _suffix(data)
+    s, n = _sort_keys(data)
     f = _fn(f"ak_merge_sort_{s}", [_P, _P, _U64, _P, _U64, C.c_int])
-    _check(f(e.handle, _ptr(data), data.numel(), _ptr(scratch), scratch.numel(), _desc(cmp)))
+    _check(f(e.handle, _ptr(data), n, _ptr(scratch), _sort_keys(scratch)[1], _desc(cmp)))
 
 
 def merge_sort_copy(data: torch.Tensor, ex: ExecBackend | None = None, cmp=None) -> torch.Tensor:
@@ -352,9 +365,10 @@ def merge_sort_by_key(keys: torch.Tensor, payload: torch.Tensor, buffers=None,
     w = payload.element_size()
     if w not in (4, 8) or sp.element_size() != w:
         raise InvalidArgument("merge_sort_by_key: payload must be 4- or 8-byte elements")
-    f = _fn(f"ak_merge_sort_by_key_{_suffix(keys)}_b{8 * w}",
+    ks, kn = _sort_keys(keys)
+    f = _fn(f"ak_merge_sort_by_key_{ks}_b{8 * w}",
             [_P, _P, _U64, _P, _U64, _P, _U64, _P, _U64, C.c_int])
-    _check(f(e.handle, _ptr(keys), keys.numel(), _ptr(payload), payload.numel(), _ptr(sk), sk.numel(),
+    _check(f(e.handle, _ptr(keys), kn, _ptr(payload), payload.numel(), _ptr(sk), _sort_keys(sk)[1],
              _ptr(sp), sp.numel(), _desc(cmp)))
 
 
@@ -371,16 +385,16 @@ def sortperm(data: torch.Tensor, out: torch.Tensor | None = None, buffers: Sortp
     """Stable index permutation (sort.hpp:238-262); equal keys keep ascending indices."""
     _dev(data, "sortperm")
     e = _ex(ex, data)
-    n = data.numel()
+    ks, n = _sort_keys(data)
     if out is None:
         out = torch.empty(n, dtype=index_dtype, device=data.device)
     if buffers is None:
         buffers = SortpermBuffers(torch.empty_like(data), torch.empty_like(data),
                                   torch.empty(n, dtype=out.dtype, device=data.device))
     isuf = _index_suffix(out.dtype)
-    f = _fn(f"ak_sortperm_{_suffix(data)}_{isuf}", [_P, _P, _U64, _P, _U64, _P, _U64, _P, _U64, _P, _U64, C.c_int])
+    f = _fn(f"ak_sortperm_{ks}_{isuf}", [_P, _P, _U64, _P, _U64, _P, _U64, _P, _U64, _P, _U64, C.c_int])
     _check(f(e.handle, _ptr(data), n, _ptr(out), out.numel(), _ptr(buffers.working_keys),
-             buffers.working_keys.numel(), _ptr(buffers.scratch_keys), buffers.scratch_keys.numel(),
+             _sort_keys(buffers.working_keys)[1], _ptr(buffers.scratch_keys), _sort_keys(buffers.scratch_keys)[1],
              _ptr(buffers.scratch_index), buffers.scratch_index.numel(), _desc(cmp)))
     return out
 
@@ -391,13 +405,13 @@ def sortperm_lowmem(data: torch.Tensor, out: torch.Tensor | None = None,
     """Low-memory sortperm (sort.hpp:267-290): index scratch only, keys gathered per pass."""
     _dev(data, "sortperm_lowmem")
     e = _ex(ex, data)
-    n = data.numel()
+    ks, n = _sort_keys(data)
     if out is None:
         out = torch.empty(n, dtype=index_dtype, device=data.device)
     if buffers is None:
         buffers = SortpermLowmemBuffers(torch.empty(n, dtype=out.dtype, device=data.device))
     isuf = _index_suffix(out.dtype)
-    f = _fn(f"ak_sortperm_lowmem_{_suffix(data)}_{isuf}", [_P, _P, _U64, _P, _U64, _P, _U64, C.c_int])
+    f = _fn(f"ak_sortperm_lowmem_{ks}_{isuf}", [_P, _P, _U64, _P, _U64, _P, _U64, C.c_int])
     _check(f(e.handle, _ptr(data), n, _ptr(out), out.numel(), _ptr(buffers.scratch_index),
              buffers.scratch_index.numel(), _desc(cmp)))
     return out

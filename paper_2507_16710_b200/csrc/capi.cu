@@ -14,6 +14,7 @@
 #include "ctx.cuh"
 #include "radix_sort.cuh"
 #include "sortperm_fast.cuh"
+#include "wide_keys.cuh"
 #include "predicates.cuh"
 #include "reduce_scan.cuh"
 #include "search_merge.cuh"
@@ -427,6 +428,52 @@ void accumulate_all_impl(ak_ctx* c, ak_comm* comm, const T* x, uint64_t n, T* ou
 
 }  // namespace
 
+// ---- int16 / int128 keys (dtype.hpp:14-21): sort family only, same argument checks ----
+template <typename T>
+void wide_merge_sort_impl(ak_ctx* c, T* data, std::uint64_t n, T* scratch, std::uint64_t scratch_n, int desc) {
+    ctx_lock g(c);
+    need(scratch_n >= n, "merge_sort: scratch buffer too small");  // sort.hpp:182-184
+    need(n == 0 || (data && scratch), "merge_sort: null buffer");
+    if (n >= 2) akb::wide_merge_sort<T>(c, data, n, desc != 0);
+    akb::ctx_finish(c);
+}
+template <typename T>
+void wide_merge_sort_host_impl(ak_ctx* c, T* h, std::uint64_t n, int desc) {
+    ctx_lock g(c);
+    need(n == 0 || h, "merge_sort: null buffer");
+    if (n < 2) return;
+    T* d = static_cast<T*>(akb::ctx_stage(c, n * sizeof(T)));
+    AKB_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    akb::wide_merge_sort<T>(c, d, n, desc != 0);
+    AKB_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));
+}
+template <typename T, typename V>
+void wide_by_key_impl(ak_ctx* c, T* keys, std::uint64_t nk, void* payload, std::uint64_t np, T* sk,
+                      std::uint64_t skn, void* sp, std::uint64_t spn, int desc) {
+    ctx_lock g(c);
+    need(nk == np, "merge_sort_by_key: keys and payload lengths differ");            // sort.hpp:214-216
+    need(skn >= nk && spn >= nk, "merge_sort_by_key: scratch buffers too small");  // :217-219
+    need(nk == 0 || (keys && payload && sk && sp), "merge_sort_by_key: null buffer");
+    if (nk >= 2) akb::wide_by_key<T, V>(c, keys, static_cast<V*>(payload), nk, desc != 0);
+    akb::ctx_finish(c);
+}
+template <typename T, typename I>
+void wide_sortperm_impl(ak_ctx* c, const T* data, std::uint64_t n, I* out, std::uint64_t out_n, std::uint64_t wkn,
+                        std::uint64_t skn, std::uint64_t sin_, bool lowmem, int desc) {
+    ctx_lock g(c);
+    need(out_n == n, lowmem ? "sortperm_lowmem: output length must match input length"
+                            : "sortperm: output length must match input length");  // sort.hpp:242-244, :270-272
+    need(lowmem ? sin_ >= n : (wkn >= n && skn >= n && sin_ >= n),
+         lowmem ? "sortperm_lowmem: scratch buffer too small" : "sortperm: scratch buffers too small");
+    need(n <= static_cast<std::uint64_t>(std::numeric_limits<I>::max()), "sortperm: index type too narrow");
+    need(n == 0 || (data && out), "sortperm: null buffer");
+    using V = std::make_unsigned_t<I>;
+    if (n == 1) AKB_CUDA(cudaMemsetAsync(out, 0, sizeof(I), c->stream));
+    else if (n > 1) akb::wide_sortperm<T, V>(c, data, n, reinterpret_cast<V*>(out), desc != 0);
+    akb::ctx_finish(c);
+}
+
 extern "C" {
 
 const char* ak_last_error(void) { return g_err.c_str(); }
@@ -638,6 +685,41 @@ AK_DEFINE(i64, int64_t)
 AK_DEFINE(u64, uint64_t)
 AK_DEFINE(f32, float)
 AK_DEFINE(f64, double)
+
+#define AK_DEFINE_WIDE(S, T)                                                                            \
+    int ak_merge_sort_##S(ak_ctx* c, T* d, uint64_t n, T* s, uint64_t sn, int desc) {                   \
+        return guard([&] { wide_merge_sort_impl<T>(c, d, n, s, sn, desc); });                           \
+    }                                                                                                    \
+    int ak_merge_sort_host_##S(ak_ctx* c, T* h, uint64_t n, int desc) {                                 \
+        return guard([&] { wide_merge_sort_host_impl<T>(c, h, n, desc); });                              \
+    }                                                                                                    \
+    int ak_merge_sort_by_key_##S##_b32(ak_ctx* c, T* k, uint64_t nk, void* p, uint64_t np, T* sk,       \
+                                       uint64_t skn, void* sp, uint64_t spn, int desc) {                \
+        return guard([&] { wide_by_key_impl<T, std::uint32_t>(c, k, nk, p, np, sk, skn, sp, spn, desc); }); \
+    }                                                                                                    \
+    int ak_merge_sort_by_key_##S##_b64(ak_ctx* c, T* k, uint64_t nk, void* p, uint64_t np, T* sk,       \
+                                       uint64_t skn, void* sp, uint64_t spn, int desc) {                \
+        return guard([&] { wide_by_key_impl<T, std::uint64_t>(c, k, nk, p, np, sk, skn, sp, spn, desc); }); \
+    }                                                                                                    \
+    int ak_sortperm_##S##_i32(ak_ctx* c, const T* d, uint64_t n, int32_t* o, uint64_t on, T*,           \
+                              uint64_t wkn, T*, uint64_t skn, int32_t*, uint64_t sin_, int desc) {       \
+        return guard([&] { wide_sortperm_impl<T, std::int32_t>(c, d, n, o, on, wkn, skn, sin_, false, desc); }); \
+    }                                                                                                    \
+    int ak_sortperm_##S##_i64(ak_ctx* c, const T* d, uint64_t n, int64_t* o, uint64_t on, T*,           \
+                              uint64_t wkn, T*, uint64_t skn, int64_t*, uint64_t sin_, int desc) {       \
+        return guard([&] { wide_sortperm_impl<T, std::int64_t>(c, d, n, o, on, wkn, skn, sin_, false, desc); }); \
+    }                                                                                                    \
+    int ak_sortperm_lowmem_##S##_i32(ak_ctx* c, const T* d, uint64_t n, int32_t* o, uint64_t on,        \
+                                     int32_t*, uint64_t sin_, int desc) {                               \
+        return guard([&] { wide_sortperm_impl<T, std::int32_t>(c, d, n, o, on, 0, 0, sin_, true, desc); }); \
+    }                                                                                                    \
+    int ak_sortperm_lowmem_##S##_i64(ak_ctx* c, const T* d, uint64_t n, int64_t* o, uint64_t on,        \
+                                     int64_t*, uint64_t sin_, int desc) {                               \
+        return guard([&] { wide_sortperm_impl<T, std::int64_t>(c, d, n, o, on, 0, 0, sin_, true, desc); }); \
+    }
+
+AK_DEFINE_WIDE(i16, int16_t)
+AK_DEFINE_WIDE(i128, ak_int128)
 
 #define AK_DEFINE_DIST(S, T)                                                                               \
     int ak_reduce_all_##S(ak_ctx* c, ak_comm* cm, const T* x, uint64_t n, int op, int map, T init, T* r) {    \
