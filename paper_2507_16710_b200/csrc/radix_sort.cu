@@ -22,6 +22,7 @@
 
 #include "radix_sort.cuh"
 #include "msd_pass.cuh"
+#include "search_merge.cuh"
 
 namespace akb {
 
@@ -1098,6 +1099,170 @@ struct lc_smem {
     static constexpr int MINB = total + 1024 <= 114 * 1024 ? 2 : 1;  // CTAs per SM that fit
 };
 
+// The counting stage of one range whose keys are in registers (k[i] = key i*LC_BLOCK + tid;
+// padding repeats a valid key) and whose per-warp min / max partials of the ordered keys are
+// in s_red[0..15] / s_red[16..31] (written before the caller's barrier): bins, ranks, and stores key j of the sorted range to out[j]. Returns 1
+// (nothing stored) when a bin overflows LC_MAX_BIN. Ends with a barrier; block-uniform.
+template <typename T, int ITEMS, bool DESC, bool MINMAX>
+__device__ __forceinline__ int count_sort_store(const T (&k)[ITEMS], std::uint32_t len, int nb_want, T* __restrict__ out,
+                                                bool copy_equal, T* s_stage, std::uint32_t* s_cw,
+                                                typename key_traits<T>::bits* s_red, std::uint32_t* s_wsum) {
+    using B = typename key_traits<T>::bits;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    std::uint16_t* s_c16 = reinterpret_cast<std::uint16_t*>(s_cw);
+    // MINMAX: lanes 0-15 fold the min partials, lanes 16-31 the max partials, and bins are
+    // taken from the OFFSET to the minimum, so a range straddling an aligned boundary
+    // (0x0fff.. | 0x1000..) still spreads over all bins (value tiles of the P-way merge).
+    // Otherwise OR / AND partials of the raw bits (bucket ranges of the sort, aligned by
+    // construction; cheaper to reduce): vary = the bits that differ, kmin = 0.
+    B kmin = 0, vary;
+    {
+        B x = s_red[lane];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const B y = __shfl_xor_sync(FULL, x, o);
+            if constexpr (MINMAX) x = lane < 16 ? (y < x ? y : x) : (y > x ? y : x);
+            else x = lane < 16 ? (x | y) : (x & y);
+        }
+        const B lo = __shfl_sync(FULL, x, 0), hi = __shfl_sync(FULL, x, 16);
+        if constexpr (MINMAX) {
+            kmin = lo;
+            vary = hi - lo;
+        } else {
+            vary = lo & ~hi;
+        }
+    }
+    if (vary == 0) {  // every key equal: the range is already sorted
+        if (copy_equal)
+            for (std::uint32_t j = tid; j < len; j += LC_BLOCK) out[j] = k[0];
+        __syncthreads();  // s_red is rewritten by the next range
+        return 0;
+    }
+    int hb;
+    if constexpr (sizeof(B) == 8) hb = 63 - __clzll(static_cast<long long>(vary));
+    else hb = 31 - __clz(static_cast<int>(vary));
+    const int nb = max(1, min(nb_want, hb + 1));
+    const int shift = hb + 1 - nb;
+    const std::uint32_t bmask = (1u << nb) - 1u;
+    const std::uint32_t nwords = 1u << (nb - 1);
+
+    // bin | slot << 16 per key: one shared atomic per key on its bin's half of a word
+    std::uint32_t pk[ITEMS];
+    bool over = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool ok = static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len;
+        const std::uint32_t bn = static_cast<std::uint32_t>((ordered(k[i], DESC) - kmin) >> shift) & bmask;
+        const std::uint32_t sh = (bn & 1u) * 16u;
+        const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
+        const std::uint32_t slot = (old >> sh) & 0xffffu;
+        over |= ok && slot >= LC_MAX_BIN;
+        pk[i] = bn | (slot << 16);
+    }
+    if (__syncthreads_or(over)) return 1;  // clustered keys: the caller hands the range on
+    // exclusive scan of the packed counts -> packed u16 bin starts. Warp w owns words
+    // [w*WPW, (w+1)*WPW), lane l the uint4 quads q*128 + 4l (conflict-free), order (q, lane).
+    {
+        const std::uint32_t wpw = nwords / LC_WARPS;  // words per warp (0 when nwords < 16)
+        const std::uint32_t nq = wpw / 128;           // full quads per lane
+        std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
+        if (nq >= 1) {
+            // up to 2 quads per lane (LC_WORDS / LC_WARPS = 256 words = 2 x 128)
+            uint4 u[2];
+            std::uint32_t cs[2] = {0, 0};
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (q < static_cast<int>(nq)) {
+                    u[q] = *reinterpret_cast<const uint4*>(wbase + q * 128);
+                    const std::uint32_t S = u[q].x + u[q].y + u[q].z + u[q].w;
+                    cs[q] = (S & 0xffffu) + (S >> 16);
+                }
+            std::uint32_t p = cs[0] | (cs[1] << 16);  // both quads' sums scanned at once
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const std::uint32_t y = __shfl_up_sync(FULL, p, o);
+                if (lane >= o) p += y;
+            }
+            const std::uint32_t t = __shfl_sync(FULL, p, 31);
+            const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
+            if (lane == 0) s_wsum[warp] = T0 + T1;
+            __syncthreads();
+            std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;  // lane-parallel warp prefix
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
+            const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (q < static_cast<int>(nq)) {
+                    std::uint32_t run = exq[q];
+                    std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u[q]);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
+                        wv[j] = run | ((run + lo) << 16);
+                        run += lo + hi;
+                    }
+                    *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
+                }
+        } else {
+            // small tables (<= 1024 words): thread t owns words [wpt*t, wpt*t + wpt), wpt <= 2
+            const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
+            const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
+            const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
+            const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
+            const std::uint32_t S = c0 + c1;
+            const std::uint32_t sum = (S & 0xffffu) + (S >> 16);
+            std::uint32_t inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            __syncthreads();
+            std::uint32_t wp = 0;
+#pragma unroll
+            for (int w = 0; w < LC_WARPS; ++w) wp += w < warp ? s_wsum[w] : 0u;
+            std::uint32_t run = wp + inc - sum;
+            if (w0 < nwords) {
+                const std::uint32_t lo = c0 & 0xffffu, hi = c0 >> 16;
+                s_cw[w0] = run | ((run + lo) << 16);
+                run += lo + hi;
+            }
+            if (wpt == 2 && w0 + 1 < nwords) s_cw[w0 + 1] = run | ((run + (c1 & 0xffffu)) << 16);
+        }
+        if (tid == 0) s_c16[2 * nwords] = static_cast<std::uint16_t>(len);  // end of the last bin
+    }
+    __syncthreads();
+    // scatter into bin order (ordered bits: ranked as unsigned)
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+        if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len)
+            reinterpret_cast<B*>(s_stage)[s_c16[pk[i] & 0xffffu] + (pk[i] >> 16)] = ordered(k[i], DESC);
+    __syncthreads();
+    // each staged position ranks its key inside its (short) bin on the full key:
+    // final slot = bin start + #(key, staged slot) lexicographically smaller
+    B* s_ord = reinterpret_cast<B*>(s_stage);
+#pragma unroll 1
+    for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
+        const B v = s_ord[x];
+        // bin extent: consecutive positions have nondecreasing bins, so a warp's counter
+        // reads fall in a few words
+        const std::uint32_t bn = static_cast<std::uint32_t>((v - kmin) >> shift) & bmask;
+        const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
+        std::uint32_t rk = x;
+        if (cnt > 1) {
+            rk = st + lex_less96(s_ord[st], st, v, x) + lex_less96(s_ord[st + 1], st + 1, v, x);
+#pragma unroll 1
+            for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(s_ord[y], y, v, x);
+        }
+        const B o = DESC ? static_cast<B>(~v) : v;
+        out[rk] = static_cast<T>(std::is_signed_v<T> ? (o ^ (B(1) << (8 * sizeof(B) - 1))) : o);
+    }
+    __syncthreads();  // the counters are read above and zeroed by the next range
+    return 0;
+}
+
 // Keys-only 64-bit integer ranges: on-chip COUNTING sort. Stability is unobservable for
 // integer keys without payload (equal keys are identical bit patterns), so the order in
 // which equal bins fill may be arbitrary. Persistent CTAs walk the ranges; a range's keys
@@ -1210,153 +1375,12 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
             __syncthreads();  // s_red is rewritten by the next range
             continue;
         }
-        // lanes 0-15 fold the OR partials, lanes 16-31 the AND partials (one load per lane)
-        B any1, all1;
-        {
-            B x = s_red[lane];
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                const B y = __shfl_xor_sync(FULL, x, o);
-                x = lane < 16 ? (x | y) : (x & y);
-            }
-            any1 = __shfl_sync(FULL, x, 0);
-            all1 = __shfl_sync(FULL, x, 16);
+        const int st_ = count_sort_store<T, ITEMS, DESC, false>(k, len, nb_want, out + b, in != out, s_stage, s_cw, s_red,
+                                                         s_wsum);
+        if (st_ == 1 && tid == 0) {  // clustered keys: hand the range to the radix kernel
+            const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(redo), 1ull);
+            redo[1 + slot] = r;
         }
-        const B vary = any1 & ~all1;
-        if (vary == 0) {  // every key equal: the range is already sorted
-            if (in != out)
-                for (std::uint32_t j = tid; j < len; j += LC_BLOCK) out[b + j] = k[0];
-            __syncthreads();
-            continue;
-        }
-        int hb;
-        if constexpr (sizeof(B) == 8) hb = 63 - __clzll(static_cast<long long>(vary));
-        else hb = 31 - __clz(static_cast<int>(vary));
-        const int nb = max(1, min(nb_want, hb + 1));
-        const int shift = hb + 1 - nb;
-        const std::uint32_t bmask = (1u << nb) - 1u;
-        const std::uint32_t nwords = 1u << (nb - 1);
-
-        // bin | slot << 16 per key: one shared atomic per key on its bin's half of a word
-        std::uint32_t pk[ITEMS];
-        bool over = false;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const bool ok = static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len;
-            const std::uint32_t bn = static_cast<std::uint32_t>(ordered(k[i], DESC) >> shift) & bmask;
-            const std::uint32_t sh = (bn & 1u) * 16u;
-            const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
-            const std::uint32_t slot = (old >> sh) & 0xffffu;
-            over |= ok && slot >= LC_MAX_BIN;
-            pk[i] = bn | (slot << 16);
-        }
-        if (__syncthreads_or(over)) {  // clustered keys: hand the range to the radix kernel
-            if (tid == 0) {
-                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(redo), 1ull);
-                redo[1 + slot] = r;
-            }
-            continue;
-        }
-        // exclusive scan of the packed counts -> packed u16 bin starts. Warp w owns words
-        // [w*WPW, (w+1)*WPW), lane l the uint4 quads q*128 + 4l (conflict-free), order (q, lane).
-        {
-            const std::uint32_t wpw = nwords / LC_WARPS;  // words per warp (0 when nwords < 16)
-            const std::uint32_t nq = wpw / 128;           // full quads per lane
-            std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
-            if (nq >= 1) {
-                // up to 2 quads per lane (LC_WORDS / LC_WARPS = 256 words = 2 x 128)
-                uint4 u[2];
-                std::uint32_t cs[2] = {0, 0};
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    if (q < static_cast<int>(nq)) {
-                        u[q] = *reinterpret_cast<const uint4*>(wbase + q * 128);
-                        const std::uint32_t S = u[q].x + u[q].y + u[q].z + u[q].w;
-                        cs[q] = (S & 0xffffu) + (S >> 16);
-                    }
-                std::uint32_t p = cs[0] | (cs[1] << 16);  // both quads' sums scanned at once
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const std::uint32_t y = __shfl_up_sync(FULL, p, o);
-                    if (lane >= o) p += y;
-                }
-                const std::uint32_t t = __shfl_sync(FULL, p, 31);
-                const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
-                if (lane == 0) s_wsum[warp] = T0 + T1;
-                __syncthreads();
-                std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;  // lane-parallel warp prefix
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
-                const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    if (q < static_cast<int>(nq)) {
-                        std::uint32_t run = exq[q];
-                        std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u[q]);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
-                            wv[j] = run | ((run + lo) << 16);
-                            run += lo + hi;
-                        }
-                        *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
-                    }
-            } else {
-                // small tables (<= 1024 words): thread t owns words [wpt*t, wpt*t + wpt), wpt <= 2
-                const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
-                const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
-                const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
-                const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
-                const std::uint32_t S = c0 + c1;
-                const std::uint32_t sum = (S & 0xffffu) + (S >> 16);
-                std::uint32_t inc = sum;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                if (lane == 31) s_wsum[warp] = inc;
-                __syncthreads();
-                std::uint32_t wp = 0;
-#pragma unroll
-                for (int w = 0; w < LC_WARPS; ++w) wp += w < warp ? s_wsum[w] : 0u;
-                std::uint32_t run = wp + inc - sum;
-                if (w0 < nwords) {
-                    const std::uint32_t lo = c0 & 0xffffu, hi = c0 >> 16;
-                    s_cw[w0] = run | ((run + lo) << 16);
-                    run += lo + hi;
-                }
-                if (wpt == 2 && w0 + 1 < nwords) s_cw[w0 + 1] = run | ((run + (c1 & 0xffffu)) << 16);
-            }
-            if (tid == 0) s_c16[2 * nwords] = static_cast<std::uint16_t>(len);  // end of the last bin
-        }
-        __syncthreads();
-        // scatter into bin order (ordered bits: ranked as unsigned)
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
-            if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len)
-                reinterpret_cast<B*>(s_stage)[s_c16[pk[i] & 0xffffu] + (pk[i] >> 16)] = ordered(k[i], DESC);
-        __syncthreads();
-        // each staged position ranks its key inside its (short) bin on the full key:
-        // final slot = bin start + #(key, staged slot) lexicographically smaller
-        B* s_ord = reinterpret_cast<B*>(s_stage);
-#pragma unroll 1
-        for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
-            const B v = s_ord[x];
-            // bin extent: consecutive positions have nondecreasing bins, so a warp's counter
-            // reads fall in a few words
-            const std::uint32_t bn = static_cast<std::uint32_t>(v >> shift) & bmask;
-            const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
-            std::uint32_t rk = x;
-            if (cnt > 1) {
-                rk = st + lex_less96(s_ord[st], st, v, x) + lex_less96(s_ord[st + 1], st + 1, v, x);
-#pragma unroll 1
-                for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(s_ord[y], y, v, x);
-            }
-            const B o = DESC ? static_cast<B>(~v) : v;
-            out[b + rk] = static_cast<T>(std::is_signed_v<T> ? (o ^ (B(1) << (8 * sizeof(B) - 1))) : o);
-        }
-        __syncthreads();  // the counters are read above and zeroed by the next range
     }  // ranges
 }
 
@@ -1436,6 +1460,156 @@ void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     c->kernel_launches += 1;
+}
+
+// ---------------------------------------------------------------------------
+// Keys-only 64-bit integer P-way merge (SIHSort's second local step): the output is cut
+// into value tiles [b_j, b_{j+1}) (b_j from a sorted sample of every run); tile j is the
+// union of one contiguous piece per run (lower_bound of b_j, b_{j+1} in each run), so it is
+// sorted on chip by the counting stage above and stored at its output offset (the number of
+// keys below b_j). Equal integer keys are indistinguishable, so this equals the stable merge.
+// ---------------------------------------------------------------------------
+constexpr int MC_MAXP = 16;
+
+template <typename T, int ITEMS>
+struct mc_smem {
+    static constexpr int CAP = LC_BLOCK * ITEMS;
+    static constexpr std::size_t stage_off = 0;
+    static constexpr std::size_t cnt_off = sizeof(T) * CAP;
+    static constexpr std::size_t red_off = cnt_off + sizeof(std::uint32_t) * (LC_WORDS + 4);
+    static constexpr std::size_t wsum_off = red_off + 2 * LC_WARPS * sizeof(std::uint64_t);
+    static constexpr std::size_t piece_off = wsum_off + 2 * LC_WARPS * sizeof(std::uint32_t);
+    static constexpr std::size_t total = piece_off + 3 * (MC_MAXP + 1) * sizeof(std::uint64_t);
+};
+
+template <typename T, int ITEMS, bool DESC>
+__global__ void __launch_bounds__(LC_BLOCK, 2)
+    merge_count_kernel(const T* const* __restrict__ runs, int P, const std::uint64_t* __restrict__ pos, T* __restrict__ dst,
+                       std::uint64_t* big) {
+    using L = mc_smem<T, ITEMS>;
+    using B = typename key_traits<T>::bits;
+    constexpr int CAP = L::CAP;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* s_stage = reinterpret_cast<T*>(smem + L::stage_off);
+    std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + L::cnt_off);
+    B* s_red = reinterpret_cast<B*>(smem + L::red_off);
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    std::uint64_t* s_lo = reinterpret_cast<std::uint64_t*>(smem + L::piece_off);  // piece start in its run
+    std::uint64_t* s_pre = s_lo + (MC_MAXP + 1);                                   // prefix of piece lengths
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const std::uint64_t j = blockIdx.x;
+    if (tid == 0) {
+        std::uint64_t acc = 0, off = 0;
+        for (int r = 0; r < P; ++r) {
+            const std::uint64_t lo = pos[j * P + r], hi = pos[(j + 1) * P + r];
+            s_lo[r] = lo;
+            s_pre[r] = acc;
+            acc += hi - lo;
+            off += lo;
+        }
+        s_pre[P] = acc;
+        s_pre[MC_MAXP + 1 + 0] = off;  // output offset of the tile
+    }
+    __syncthreads();
+    const std::uint64_t total = s_pre[P], off = s_pre[MC_MAXP + 1];
+    if (total == 0) return;
+    if (total > static_cast<std::uint64_t>(CAP)) {
+        if (tid == 0) {
+            const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+            big[1 + slot] = j;
+        }
+        return;
+    }
+    const std::uint32_t len = static_cast<std::uint32_t>(total);
+    T k[ITEMS];
+    B orv = static_cast<B>(~B(0)), andv = 0;  // min / max of the ordered keys
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const std::uint32_t li = static_cast<std::uint32_t>(i * LC_BLOCK + tid);
+        const std::uint32_t lj = li < len ? li : 0u;
+        int r = 0;
+        for (int q = 1; q < P; ++q) r += (s_pre[q] <= lj) ? 1 : 0;
+        k[i] = runs[r][s_lo[r] + (lj - s_pre[r])];
+        const B o = ordered(k[i], DESC);
+        orv = o < orv ? o : orv;
+        andv = o > andv ? o : andv;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const B y0 = __shfl_xor_sync(FULL, orv, o), y1 = __shfl_xor_sync(FULL, andv, o);
+        orv = y0 < orv ? y0 : orv;
+        andv = y1 > andv ? y1 : andv;
+    }
+    if (lane == 0) {
+        s_red[warp] = orv;
+        s_red[LC_WARPS + warp] = andv;
+    }
+    const int nb_want = min(LC_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
+    const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
+    if (nwords_w >= 4) {
+        for (int i = tid; i < nwords_w / 4; i += LC_BLOCK) reinterpret_cast<uint4*>(s_cw)[i] = make_uint4(0, 0, 0, 0);
+    } else if (tid < nwords_w) {
+        s_cw[tid] = 0;
+    }
+    __syncthreads();
+    if (count_sort_store<T, ITEMS, DESC, true>(k, len, nb_want, dst + off, true, s_stage, s_cw, s_red, s_wsum) == 1 &&
+        tid == 0) {
+        const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+        big[1 + slot] = j;
+    }
+}
+
+// samples[so[r] + i] = run r at i * S (the run's first key included)
+template <typename T>
+__global__ void mc_sample_kernel(const T* const* __restrict__ runs, const std::uint64_t* __restrict__ so, int P,
+                                 std::uint32_t S, T* __restrict__ samples) {
+    const std::uint64_t M = so[P];
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t x = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < M; x += stride) {
+        int r = 0;
+        while (r + 1 < P && so[r + 1] <= x) ++r;
+        samples[x] = runs[r][(x - so[r]) * S];
+    }
+}
+
+// pos[j * P + r] = lower_bound(run r, b_j) with b_j = sorted[j * K]; row 0 = 0, row J = lens;
+// mx = largest tile.
+template <typename T>
+__global__ void mc_bounds_kernel(const T* const* __restrict__ runs, const std::uint64_t* __restrict__ lens, int P,
+                                 const T* __restrict__ sorted, std::uint64_t J, std::uint32_t K, int desc,
+                                 std::uint64_t* __restrict__ pos) {
+    const std::uint64_t x = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (x >= (J + 1) * P) return;
+    const std::uint64_t j = x / P;
+    const int r = static_cast<int>(x % P);
+    const std::uint64_t n = lens[r];
+    if (j == 0 || j == J) {
+        pos[x] = j == 0 ? 0 : n;
+        return;
+    }
+    const T v = sorted[j * K];
+    const T* h = runs[r];
+    std::uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const std::uint64_t mid = lo + (hi - lo) / 2;
+        if (key_less(h[mid], v, desc != 0)) lo = mid + 1;
+        else hi = mid;
+    }
+    pos[x] = lo;
+}
+
+__global__ void mc_maxtile_kernel(const std::uint64_t* __restrict__ pos, int P, std::uint64_t J,
+                                  unsigned long long* __restrict__ mx) {
+    const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    std::uint64_t t = 0;
+    if (j < J)
+        for (int r = 0; r < P; ++r) t += pos[(j + 1) * P + r] - pos[j * P + r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const std::uint64_t y = __shfl_xor_sync(FULL, t, o);
+        t = t > y ? t : y;
+    }
+    if ((threadIdx.x & 31) == 0 && t) atomicMax(mx, static_cast<unsigned long long>(t));
 }
 
 int local_count_env() {
@@ -1701,7 +1875,115 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
     else return false;
 }
 
+int merge_count_env() {
+    static const int v = [] {
+        const char* e = std::getenv("AKB_MERGE_COUNT");  // "0": always the merge-path tree
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+template <typename T>
+bool merge_runs_counting_impl(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* lens, T* dst, bool desc) {
+    constexpr int ITEMS = 9;  // 4608-key tiles, two CTAs per SM
+    using MS = mc_smem<T, ITEMS>;
+    constexpr std::uint32_t CAPK = MS::CAP;
+    std::uint64_t n = 0;
+    for (int r = 0; r < P; ++r) n += lens[r];
+    // P = 8, 2^28 int64: 3.70 -> 2.83 ms; P = 4: break-even with the 2-level tree (2.44 ms)
+    if (merge_count_env() == 0 || P < 6 || P > MC_MAXP || n < (std::uint64_t(1) << 22)) return false;
+    // sample stride S with (K + P) * S <= CAP (the largest possible tile without heavy ties)
+    // sample stride S and tile width K (samples): a tile holds at most (K + P) * S keys (each
+    // run adds at most one partial sample block), expected K * S
+    const std::uint32_t S = 128;
+    const std::uint32_t K = CAPK / S - static_cast<std::uint32_t>(P);
+    std::vector<std::uint64_t> so(P + 1, 0);
+    for (int r = 0; r < P; ++r) so[r + 1] = so[r] + (lens[r] + S - 1) / S;
+    const std::uint64_t M = so[P];
+    const std::uint64_t J = (M + K - 1) / K;
+    // arena: [P run ptrs][P lens][P+1 sample offsets][M samples][M scratch][(J+1)P pos][1 max]
+    //        [CAP tile scratch for the clustered-tile fallback]
+    const std::size_t words = 3 * P + 1 + 2 * M + (J + 1) * P + 1 + CAPK;
+    auto* w = static_cast<std::uint64_t*>(ctx_work(c, words * sizeof(std::uint64_t)));
+    if (!w) return false;
+    auto* d_runs = reinterpret_cast<const T**>(w);
+    std::uint64_t* d_lens = w + P;
+    std::uint64_t* d_so = w + 2 * P;
+    T* samples = reinterpret_cast<T*>(w + 3 * P + 1);
+    T* sscr = samples + M;
+    std::uint64_t* pos = w + 3 * P + 1 + 2 * M;
+    std::uint64_t* mx = pos + (J + 1) * P;
+    auto* h = static_cast<std::uint64_t*>(ctx_pinned(c, (3 * P + 1) * sizeof(std::uint64_t)));
+    for (int r = 0; r < P; ++r) {
+        h[r] = reinterpret_cast<std::uint64_t>(runs[r]);
+        h[P + r] = lens[r];
+    }
+    for (int r = 0; r <= P; ++r) h[2 * P + r] = so[r];
+    AKB_CUDA(cudaMemcpyAsync(w, h, (3 * P + 1) * sizeof(std::uint64_t), cudaMemcpyHostToDevice, c->stream));
+    mc_sample_kernel<T><<<c->sm_count * 4, 256, 0, c->stream>>>(d_runs, d_so, P, S, samples);
+    AKB_CUDA(cudaGetLastError());
+    radix_sort<T, std::uint32_t>(c, SORT_KEYS, samples, samples, sscr, nullptr, nullptr, nullptr, M, desc, true);
+    mc_bounds_kernel<T><<<static_cast<unsigned>(ceil_div((J + 1) * P, 256)), 256, 0, c->stream>>>(
+        d_runs, d_lens, P, samples, J, K, desc ? 1 : 0, pos);
+    AKB_CUDA(cudaMemsetAsync(mx, 0, sizeof(std::uint64_t), c->stream));
+    mc_maxtile_kernel<<<static_cast<unsigned>(ceil_div(J, 256)), 256, 0, c->stream>>>(
+        pos, P, J, reinterpret_cast<unsigned long long*>(mx));
+    AKB_CUDA(cudaGetLastError());
+    AKB_CUDA(cudaMemcpyAsync(h, mx, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));
+    if (h[0] > CAPK) return false;  // heavy ties: the merge-path tree
+    std::uint64_t* big = ctx_cuts(c, J + 2);
+    AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
+    static bool configured = false;
+    if (!configured) {
+        AKB_CUDA(cudaFuncSetAttribute(merge_count_kernel<T, ITEMS, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(MS::total)));
+        AKB_CUDA(cudaFuncSetAttribute(merge_count_kernel<T, ITEMS, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(MS::total)));
+        configured = true;
+    }
+    const int tok = ctx_prof_begin(c, KF_MERGE);
+    if (desc)
+        merge_count_kernel<T, ITEMS, true><<<static_cast<unsigned>(J), LC_BLOCK, MS::total, c->stream>>>(d_runs, P, pos,
+                                                                                                      dst, big);
+    else
+        merge_count_kernel<T, ITEMS, false><<<static_cast<unsigned>(J), LC_BLOCK, MS::total, c->stream>>>(d_runs, P,
+                                                                                                       pos, dst, big);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 5;
+    // clustered tiles (a bin over LC_MAX_BIN): the caller's tree merges them piece-wise
+    AKB_CUDA(cudaMemcpyAsync(h, big, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));
+    const std::uint64_t nbig = h[0];
+    if (nbig) {
+        std::vector<std::uint64_t> ids(nbig), hp((J + 1) * P);
+        AKB_CUDA(cudaMemcpy(ids.data(), big + 1, nbig * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+        AKB_CUDA(cudaMemcpy(hp.data(), pos, hp.size() * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+        T* tscr = reinterpret_cast<T*>(mx + 1);  // tiles here hold <= CAP keys
+        for (std::uint64_t j : ids) {
+            std::vector<const T*> pp(P);
+            std::vector<std::uint64_t> pl(P);
+            std::uint64_t off = 0, tot = 0;
+            for (int r = 0; r < P; ++r) {
+                pp[r] = runs[r] + hp[j * P + r];
+                pl[r] = hp[(j + 1) * P + r] - hp[j * P + r];
+                off += hp[j * P + r];
+                tot += pl[r];
+            }
+            merge_runs<T>(c, P, pp.data(), pl.data(), dst + off, tscr, desc);
+        }
+    }
+    return true;
+}
+
 }  // namespace
+
+template <typename T>
+bool merge_runs_counting(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* lens, T* dst, bool desc) {
+    if constexpr (std::is_integral_v<T> && sizeof(T) == 8) return merge_runs_counting_impl<T>(c, P, runs, lens, dst, desc);
+    else return false;
+}
 
 template <typename T, typename V>
 void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vin, V* vout, V* valt,
@@ -1743,6 +2025,9 @@ std::uint64_t radix_tile_items(int key_bytes, int) {
 #define AKB_INST_K(T)          \
     AKB_INST(T, std::uint32_t) \
     AKB_INST(T, std::uint64_t)
+
+template bool merge_runs_counting<std::int64_t>(ak_ctx*, int, const std::int64_t* const*, const std::uint64_t*, std::int64_t*, bool);
+template bool merge_runs_counting<std::uint64_t>(ak_ctx*, int, const std::uint64_t* const*, const std::uint64_t*, std::uint64_t*, bool);
 
 AKB_INST_K(std::int32_t)
 AKB_INST_K(std::uint32_t)

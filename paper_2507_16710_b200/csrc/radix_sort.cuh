@@ -41,4 +41,9 @@ void radix_sort(ak_ctx* c, int mode, const T* kin, T* kout, T* kalt, const V* vi
 // none -- look-back and histograms live in the ctx. Exposed for documentation.
 std::uint64_t radix_tile_items(int key_bytes, int mode);
 
+// Keys-only 64-bit integer P-way merge (6 <= P <= 16, >= 2^22 keys) by value tiles sorted on
+// chip; returns false (nothing done) when it does not apply. Used by merge_runs.
+template <typename T>
+bool merge_runs_counting(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* lens, T* dst, bool desc);
+
 }  // namespace akb

@@ -1,5 +1,6 @@
 // search_merge.cu -- searchsorted, sample gather, merge-path 2-way merge, is_sorted.
 #include "search_merge.cuh"
+#include "radix_sort.cuh"
 
 #include <vector>
 
@@ -210,6 +211,16 @@ void merge_runs(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* len
         if (live[0].p != dst)
             AKB_CUDA(cudaMemcpyAsync(dst, live[0].p, live[0].len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
         return;
+    }
+    if constexpr (std::is_integral_v<T> && sizeof(T) == 8) {
+        // keys-only 64-bit integers, P >= 6: one pass over value tiles (radix_sort.cu)
+        std::vector<const T*> rp;
+        std::vector<std::uint64_t> rl;
+        for (const run& x : live) {
+            rp.push_back(x.p);
+            rl.push_back(x.len);
+        }
+        if (merge_runs_counting<T>(c, static_cast<int>(live.size()), rp.data(), rl.data(), dst, desc)) return;
     }
     int levels = 0;
     for (std::size_t m = 1; m < live.size(); m <<= 1) ++levels;

@@ -65,3 +65,28 @@ def test_merge_runs_descending(ak, ex, dev):
     runs = [np.sort(rng.integers(-1000, 1000, 30_000))[::-1].copy() for _ in range(5)]
     got = ak.merge_runs([torch.from_numpy(r).to(dev) for r in runs], ex=ex, cmp="greater").cpu().numpy()
     assert np.array_equal(got, np.sort(np.concatenate(runs))[::-1])
+
+
+@pytest.mark.parametrize("P", [6, 8, 16])
+@pytest.mark.parametrize("kind", ["uniform", "ties", "narrow"])
+def test_merge_runs_value_tiles_int64(ak, ex, dev, P, kind):
+    """P >= 6 int64 runs >= 2^22 keys take the one-pass value-tile merge (radix_sort.cu,
+    merge_runs_counting); ties and narrow ranges exercise the clustered-tile fallback."""
+    n = (1 << 22) + 12345
+    g = torch.Generator(device=dev).manual_seed(P)
+    if kind == "uniform":
+        x = torch.randint(-(1 << 62), 1 << 62, (n,), device=dev, generator=g)
+    elif kind == "ties":
+        x = torch.randint(0, 5000, (n,), device=dev, generator=g) * 1000003
+    else:
+        x = torch.randint(-300, 300, (n,), device=dev, generator=g) + (1 << 40)
+    cuts = sorted(torch.randint(0, n, (P - 1,), generator=torch.Generator().manual_seed(P)).tolist())
+    bounds = [0] + cuts + [n]
+    runs = [torch.sort(x[bounds[r]:bounds[r + 1]])[0] for r in range(P)]
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    ak.merge_runs(runs, out=out, scratch=torch.empty_like(out), ex=ex)
+    assert torch.equal(out, torch.sort(x)[0])
+    for r in runs:  # descending
+        r.copy_(torch.flip(r, [0]))
+    ak.merge_runs(runs, out=out, scratch=torch.empty_like(out), ex=ex, cmp="greater")
+    assert torch.equal(out, torch.sort(x, descending=True)[0])
