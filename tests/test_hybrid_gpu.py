@@ -109,3 +109,25 @@ def test_hybrid_three_level_msd(ak, ex, dev, n):
     del s
     assert bool((x[1:] >= x[:-1]).all())
     assert _fingerprint(x) == fp
+
+
+@pytest.mark.parametrize("kind", ["uniform", "low40", "dups", "cluster", "midconst", "sorted"])
+@pytest.mark.parametrize("desc", [False, True])
+def test_msd_path_distributions(ak, ex, dev, kind, desc):
+    # n >= 2^24: the unstable MSD partition passes (msd_pass.cu) before the local stage,
+    # both directions, skewed inputs (exact-largest-bucket range sizing, oversized ranges)
+    n = (1 << 24) + 77
+    x = dist(np.random.default_rng(24 + len(kind)), n, kind)
+    d = torch.from_numpy(x).to(dev)
+    ak.merge_sort(d, ex=ex, cmp="greater" if desc else None)
+    want = np.sort(x)
+    assert np.array_equal(d.cpu().numpy(), want[::-1] if desc else want)
+
+
+def test_msd_path_uint64_out_of_place(ak, ex, dev):
+    n = (1 << 24) + 5
+    x = dist(np.random.default_rng(7), n, "uniform", np.uint64)
+    d = torch.from_numpy(x.view(np.int64)).to(dev).view(torch.uint64)
+    y = ak.merge_sort_copy(d, ex=ex, cmp="greater")
+    assert np.array_equal(d.cpu().numpy().view(np.uint64), x)
+    assert np.array_equal(y.cpu().numpy().view(np.uint64), np.sort(x)[::-1])
