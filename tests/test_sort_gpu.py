@@ -184,3 +184,15 @@ def test_sortperm_composite_path_matches_oracle(ak, orc, ex, dev, dt, idx):
         want = orc.sortperm(x, descending=desc)
         p = ak.sortperm(tdev(x, dev), ex=ex, cmp="greater" if desc else None, index_dtype=idx)
         assert np.array_equal(p.cpu().numpy().astype(np.uint64), want)
+
+
+@pytest.mark.parametrize("desc", [False, True])
+def test_sortperm_composite_msd_sizes_int32(ak, ex, dev, desc):
+    """n >= 2^24 int32 sortperm: the composite 64-bit keys take the MSD partition passes too."""
+    n = (1 << 24) + 3
+    rng = np.random.default_rng(2424)
+    x = rng.integers(-(1 << 31), 1 << 31, n, dtype=np.int64).astype(np.int32)
+    x[rng.integers(0, n, 1 << 20)] = x[11]  # ties
+    want = np.argsort(-x.astype(np.int64) if desc else x, kind="stable")
+    p = ak.sortperm(torch.from_numpy(x).to(dev), ex=ex, cmp="greater" if desc else None, index_dtype=torch.int32)
+    assert np.array_equal(p.cpu().numpy(), want)
