@@ -90,7 +90,16 @@ __global__ void __launch_bounds__(MERGE_BLOCK)
                  const std::uint64_t* __restrict__ split, T* __restrict__ dst, int desc) {
     constexpr int ITEMS = merge_cfg<T>::ITEMS;
     constexpr int TILE = merge_cfg<T>::TILE;
+#ifdef AKB_MERGE_LDG
     __shared__ T s[TILE];
+#else
+    // the a- and b-pieces arrive by two TMA bulk copies of their 16-byte aligned supersets
+    // (global -> shared without a register or L1 round trip); each copy has <= 16 bytes of
+    // slack at both ends
+    constexpr int SLACK = 16 / sizeof(T);
+    __shared__ __align__(16) T s[TILE + 4 * SLACK];
+    __shared__ __align__(8) std::uint64_t bar;
+#endif
     const bool dsc = desc != 0;
     const std::uint64_t t = blockIdx.x;
     const std::uint64_t d0 = t * TILE;
@@ -99,11 +108,46 @@ __global__ void __launch_bounds__(MERGE_BLOCK)
     const std::uint64_t a0 = split[t], a1 = split[t + 1];
     const std::uint64_t b0 = d0 - a0, b1 = d1 - a1;
     const int la = static_cast<int>(a1 - a0), lb = static_cast<int>(b1 - b0);
+#ifdef AKB_MERGE_LDG
     for (int i = threadIdx.x; i < la; i += MERGE_BLOCK) s[i] = a[a0 + i];
     for (int i = threadIdx.x; i < lb; i += MERGE_BLOCK) s[la + i] = b[b0 + i];
     __syncthreads();
     const T* sa = s;
     const T* sb = s + la;
+#else
+    auto span_of = [](const T* p, std::uint64_t lo, std::uint64_t hi, std::uintptr_t& g0, std::uint32_t& bytes) {
+        const std::uintptr_t x0 = reinterpret_cast<std::uintptr_t>(p + lo), x1 = reinterpret_cast<std::uintptr_t>(p + hi);
+        g0 = x0 & ~std::uintptr_t(15);
+        bytes = static_cast<std::uint32_t>(((x1 + 15) & ~std::uintptr_t(15)) - g0);
+        return static_cast<int>((x0 - g0) / sizeof(T));  // element shift inside the copy
+    };
+    std::uintptr_t ga = 0, gb = 0;
+    std::uint32_t ba = 0, bb = 0;
+    const int sha = la ? span_of(a, a0, a1, ga, ba) : 0;
+    const int shb = lb ? span_of(b, b0, b1, gb, bb) : 0;
+    const int offb = ((la + sha + SLACK - 1) / SLACK + 1) * SLACK;  // 16-byte aligned start of the b copy
+    const std::uint32_t sbar = static_cast<std::uint32_t>(__cvta_generic_to_shared(&bar));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(ba + bb) : "memory");
+        if (ba)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             static_cast<std::uint32_t>(__cvta_generic_to_shared(s))),
+                         "l"(ga), "r"(ba), "r"(sbar)
+                         : "memory");
+        if (bb)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             static_cast<std::uint32_t>(__cvta_generic_to_shared(s + offb))),
+                         "l"(gb), "r"(bb), "r"(sbar)
+                         : "memory");
+    }
+    __syncthreads();  // barrier initialised before anyone waits
+    asm volatile("{ .reg .pred p; W_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0; @!p bra W_%=; }" ::"r"(sbar)
+                 : "memory");
+    const T* sa = s + sha;
+    const T* sb = s + offb + shb;
+#endif
     const int total = la + lb;
     T outv[ITEMS];
     const int k0 = threadIdx.x * ITEMS;
