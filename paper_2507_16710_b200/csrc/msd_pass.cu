@@ -172,12 +172,17 @@ constexpr int MP_ITEMS = AKB_MP_ITEMS;
 constexpr int MP_TILE = MP_BLOCK * MP_ITEMS;  // 8192 keys
 constexpr int MP_SPAN = 4;                    // LEVEL 2: top buckets a tile may span on chip
 constexpr int MP_BINS = 256 * MP_SPAN;
+#ifndef AKB_MP_PARTS
+#define AKB_MP_PARTS 1
+#endif
+// sub-counters per bin (lane & (PARTS-1) picks one): spreads a warp's same-bin atomics
+constexpr int MP_PARTS = AKB_MP_PARTS;
 
 struct mp_smem {
     static constexpr std::size_t stage_off = 0;
     static constexpr std::size_t stage_bytes = 8 * MP_TILE;
     static constexpr std::size_t cnt_off = stage_bytes;  // u32 counts, then local starts
-    static constexpr std::size_t gofs_off = cnt_off + 4 * MP_BINS;
+    static constexpr std::size_t gofs_off = cnt_off + 4 * MP_BINS * MP_PARTS;
     static constexpr std::size_t wsum_off = gofs_off + 8 * MP_BINS;
     static constexpr std::size_t misc_off = wsum_off + 4 * (MP_BLOCK / 32);
     static constexpr std::size_t total = misc_off + 16;
@@ -221,7 +226,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
         }
         return;
     }
-    for (std::uint32_t i = tid; i < nbins; i += MP_BLOCK) s_cnt[i] = 0;
+    for (std::uint32_t i = tid; i < nbins * MP_PARTS; i += MP_BLOCK) s_cnt[i] = 0;
 
     // load: 128-bit vectors when the tile is full and aligned
     T k[MP_ITEMS];
@@ -254,14 +259,24 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
 #pragma unroll
     for (int i = 0; i < MP_ITEMS / 2; ++i) sl[i] = 0;
 #pragma unroll
+    const std::uint32_t part = static_cast<std::uint32_t>(lane) & (MP_PARTS - 1);
     for (int i = 0; i < MP_ITEMS; ++i)
-        if (item_ok(i)) sl[i / 2] |= atomicAdd(&s_cnt[bin_of(k[i])], 1u) << (16 * (i & 1));
+        if (item_ok(i)) sl[i / 2] |= atomicAdd(&s_cnt[bin_of(k[i]) * MP_PARTS + part], 1u) << (16 * (i & 1));
     __syncthreads();
-    // bin starts (exclusive scan over <= 1024 bins, 2 per thread) + global claims
+    // bin starts: thread t owns whole bins [t*BPT, t*BPT + BPT) (BPT <= 2) and their PARTS
+    // sub-counters; exclusive scan in (bin, part) order + one global claim per non-empty bin
     {
-        const std::uint32_t b0 = 2 * tid, b1 = 2 * tid + 1;
-        const std::uint32_t c0 = b0 < nbins ? s_cnt[b0] : 0u, c1 = b1 < nbins ? s_cnt[b1] : 0u;
-        const std::uint32_t sum = c0 + c1;
+        constexpr int MAXC = 2 * MP_PARTS;
+        const std::uint32_t bpt = nbins > MP_BLOCK ? 2u : 1u;
+        const std::uint32_t fs = static_cast<std::uint32_t>(tid) * bpt * MP_PARTS;  // first sub-counter
+        const std::uint32_t nsub = nbins * MP_PARTS;
+        std::uint32_t c[MAXC];
+        std::uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q) {
+            c[q] = (static_cast<std::uint32_t>(q) < bpt * MP_PARTS && fs + q < nsub) ? s_cnt[fs + q] : 0u;
+            sum += c[q];
+        }
         std::uint32_t inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -273,26 +288,34 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
         std::uint32_t wp = 0;
 #pragma unroll
         for (int w = 0; w < MP_BLOCK / 32; ++w) wp += w < warp ? s_wsum[w] : 0u;
-        const std::uint32_t st0 = wp + inc - sum, st1 = st0 + c0;
+        std::uint32_t run = wp + inc - sum;
         // global position of staged slot j in bin b = gofs[b] + j
-        if (c0) {
-            const std::uint64_t g = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + b0),
-                                              static_cast<unsigned long long>(c0));
-            s_gofs[b0] = g - st0;
-        }
-        if (c1) {
-            const std::uint64_t g = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + b1),
-                                              static_cast<unsigned long long>(c1));
-            s_gofs[b1] = g - st1;
+        std::uint32_t r2 = run;
+#pragma unroll
+        for (int bi = 0; bi < 2; ++bi) {
+            const std::uint32_t bin = fs / MP_PARTS + bi;
+            std::uint32_t tot = 0;
+#pragma unroll
+            for (int q = 0; q < MP_PARTS; ++q) tot += c[bi * MP_PARTS + q];
+            if (static_cast<std::uint32_t>(bi) < bpt && bin < nbins && tot) {
+                const std::uint64_t g = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + bin),
+                                                  static_cast<unsigned long long>(tot));
+                s_gofs[bin] = g - r2;
+            }
+            r2 += tot;
         }
         __syncthreads();  // every count read before the starts overwrite them
-        if (b0 < nbins) s_cnt[b0] = st0;
-        if (b1 < nbins) s_cnt[b1] = st1;
+#pragma unroll
+        for (int q = 0; q < MAXC; ++q)
+            if (static_cast<std::uint32_t>(q) < bpt * MP_PARTS && fs + q < nsub) {
+                s_cnt[fs + q] = run;
+                run += c[q];
+            }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < MP_ITEMS; ++i)
-        if (item_ok(i)) s_stage[s_cnt[bin_of(k[i])] + ((sl[i / 2] >> (16 * (i & 1))) & 0xffffu)] = k[i];
+        if (item_ok(i)) s_stage[s_cnt[bin_of(k[i]) * MP_PARTS + part] + ((sl[i / 2] >> (16 * (i & 1))) & 0xffffu)] = k[i];
     __syncthreads();
     // contiguous per-bin runs: consecutive staged slots of one bin go to consecutive addresses
 #pragma unroll 4
