@@ -42,7 +42,7 @@ __device__ __forceinline__ std::uint64_t ord64(T v, bool desc) {
 // reaches JH_FLUSH is moved to the global histogram by the thread whose increment reached
 // it (at most JH_BLOCK increments can be in flight, far below the 0x10000 - JH_FLUSH of
 // headroom, so a half never carries into its neighbour).
-template <typename T>
+template <typename T, bool D5>
 __global__ void __launch_bounds__(JH_BLOCK, 1)
     hist_joint_kernel(const T* __restrict__ keys, std::uint64_t n, int desc, std::uint64_t* __restrict__ g_hist,
                       std::uint64_t* __restrict__ g_joint) {
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(JH_BLOCK, 1)
     auto count = [&](T k) {
         const std::uint64_t o = ord64(k, dsc);
         const std::uint32_t hi = static_cast<std::uint32_t>(o >> 32);
-        atomicAdd(&s_dig[((hi >> 8) & 0xffu) * JH_PARTS + part], 1u);  // digit 5 (digits 6, 7: marginals)
+        if constexpr (D5) atomicAdd(&s_dig[((hi >> 8) & 0xffu) * JH_PARTS + part], 1u);  // digit 5 (6, 7: marginals)
         const std::uint32_t bin = hi >> 16;
         const std::uint32_t sh = (bin & 1u) * 16u;
         const std::uint32_t old = atomicAdd(&s_joint[bin >> 1], 1u << sh);
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(JH_BLOCK, 1)
         if (v >> 16)
             atomicAdd(reinterpret_cast<unsigned long long*>(g_joint + 2 * w + 1), static_cast<unsigned long long>(v >> 16));
     }
-    for (int i = threadIdx.x; i < 256; i += JH_BLOCK) {
+    for (int i = threadIdx.x; D5 && i < 256; i += JH_BLOCK) {
         std::uint32_t s = 0;
 #pragma unroll
         for (int q = 0; q < JH_PARTS; ++q) s += s_dig[i * JH_PARTS + q];
@@ -440,17 +440,23 @@ __global__ void __launch_bounds__(1024) scan24_chunk_kernel(const std::uint32_t*
 }  // namespace
 
 template <typename T>
-void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint) {
+void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint,
+              bool digit5) {
     static bool configured = false;
     constexpr std::size_t smem = JOINT_BINS * 2 + 256 * JH_PARTS * 4;
     if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(hist_joint_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        AKB_CUDA(cudaFuncSetAttribute(hist_joint_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        AKB_CUDA(cudaFuncSetAttribute(hist_joint_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
         configured = true;
     }
     AKB_CUDA(cudaMemsetAsync(g_joint, 0, JOINT_BINS * sizeof(std::uint64_t), c->stream));
     const int tok = ctx_prof_begin(c, KF_HIST);
-    hist_joint_kernel<T><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
+    if (digit5)
+        hist_joint_kernel<T, true><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
+    else
+        hist_joint_kernel<T, false><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     joint_scan_kernel<<<1, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, g_joint + 2 * JOINT_BINS, g_hist);
@@ -546,9 +552,9 @@ std::uint64_t msd_max_bucket(ak_ctx* c, int level) {
 template void msd_level3<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::uint64_t, bool);
 template void msd_level3<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t, bool);
 template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t, bool, std::uint64_t*,
-                                     std::uint64_t*);
+                                     std::uint64_t*, bool);
 template void msd_hist<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t, bool, std::uint64_t*,
-                                      std::uint64_t*);
+                                      std::uint64_t*, bool);
 template void msd_top16<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::int64_t*, std::uint64_t,
                                       bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*);
 template void msd_top16<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t*, std::uint64_t,

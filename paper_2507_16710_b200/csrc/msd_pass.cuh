@@ -11,8 +11,10 @@ namespace akb {
 // One read of the keys: g_hist rows 5..7 (+=, top three 8-bit digits of the ordered key),
 // g_joint[0 .. 65536) = the histogram of the top 16 bits, and its exclusive scans:
 // g_joint[65536 + b] = start of 16-bit bucket b, g_joint[131072 + d] = start of 8-bit bucket d.
+// digit5 = false skips row 5 (the plan then reads it from a separate full histogram if needed).
 template <typename T>
-void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint);
+void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint,
+              bool digit5);
 
 // Two partition passes (kin -> kmid by the top 8 bits, kmid -> kout by the top 16 bits);
 // afterwards kout is ordered by its top 16 bits (order inside a 16-bit bucket arbitrary).

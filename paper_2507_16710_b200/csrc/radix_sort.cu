@@ -1689,9 +1689,13 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                             n >= (std::uint64_t(1) << 24);  // below: the joint-histogram flush dominates
         std::uint64_t* msdbuf = msd_ok ? ctx_msd(c) : nullptr;
         bool joint_valid = false;
+        // below 2^29 keys the plan needs only digits 7 and 6 (the joint histogram's marginals):
+        // the joint read skips digit 5, and a plan that does reach it re-reads (skewed keys)
+        const bool d5 = n >= (std::uint64_t(1) << 29);
+        if (msd_ok && !d5) first = PASSES - 2;
         auto run_hist = [&](int f) {
-            if (f == PASSES - 3 && msd_ok) {
-                msd_hist<T>(c, kin, n, desc, g_hist, msdbuf);
+            if (f != 0 && msd_ok) {
+                msd_hist<T>(c, kin, n, desc, g_hist, msdbuf, d5);
                 joint_valid = true;
                 return;
             }
