@@ -1407,6 +1407,14 @@ __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, i
     cuts[j] = lo;
 }
 
+// cuts[0] = 0, cuts[j] = ends[j - 1] (the MSD cursors after the last pass = bucket ends), cuts[J] = n.
+__global__ void cuts_from_ends_kernel(const std::uint64_t* __restrict__ ends, std::uint64_t J, std::uint64_t n,
+                                      std::uint64_t* __restrict__ cuts) {
+    const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j > J) return;
+    cuts[j] = j == 0 ? 0 : (j == J ? n : ends[j - 1]);
+}
+
 // cut b = first index whose top bits are >= b (bucket starts), b in [0, J); cuts[J] = n.
 template <typename T>
 __global__ void bucket_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
@@ -1679,6 +1687,8 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     bool bucket_mode = false;
     std::uint64_t step = n, J = 1, base_id = 0;
     const T* G = kin;  // buffer holding the bucket-ordered keys
+    std::uint64_t* msdbuf = nullptr;
+    bool used_msd = false;
     if (n > static_cast<std::uint64_t>(LOCAL_TILE)) {
         const int blocks = c->sm_count * 4;
         AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
@@ -1687,7 +1697,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         // the unstable MSD passes start their cursors from
         const bool msd_ok = msd_env() != 0 && std::is_integral_v<T> && sizeof(T) == 8 && env <= 0 &&
                             n >= (std::uint64_t(1) << 24);  // below: the joint-histogram flush dominates
-        std::uint64_t* msdbuf = msd_ok ? ctx_msd(c) : nullptr;
+        msdbuf = msd_ok ? ctx_msd(c) : nullptr;
         bool joint_valid = false;
         // below 2^29 keys the plan needs only digits 7 and 6 (the joint histogram's marginals):
         // the joint read skips digit 5, and a plan that does reach it re-reads (skewed keys)
@@ -1785,6 +1795,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
             // equal keys is unobservable)
             msd_top16<T>(c, kin, kalt, kout, n, desc, msdbuf, msdbuf + 65536, msdbuf + 2 * 65536);
             cur = kout;
+            used_msd = true;
             if (m == 3) {
                 msd_level3<T>(c, kout, kalt, n, desc);
                 cur = kalt;
@@ -1816,7 +1827,11 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     std::uint64_t* redo = big + J + 1;
     AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
     const int top_shift = 8 * (top - (m > 0 ? m : 1));
-    if (bucket_mode)
+    if (bucket_mode && used_msd && m == 2 && J == 65536)
+        // the MSD cursors end at the bucket ends: cuts[j] = end of bucket j - 1 (no search)
+        cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(msdbuf + 65536, J, n,
+                                                                                                 cuts);
+    else if (bucket_mode)
         bucket_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
             G, n, top_shift, desc ? 1 : 0, J, base_id, cuts);
     else
