@@ -167,7 +167,7 @@ std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count) {
 }
 
 std::uint64_t* ctx_msd(ak_ctx* c) {
-    if (!c->msd) AKB_CUDA(cudaMalloc(&c->msd, (2 * 65536 + 256 + 8) * sizeof(std::uint64_t)));
+    if (!c->msd) AKB_CUDA(cudaMalloc(&c->msd, (2 * 65536 + 256 + 8 + 64 + 64 * 256) * sizeof(std::uint64_t)));
     return c->msd;
 }
 

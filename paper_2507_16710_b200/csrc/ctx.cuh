@@ -110,6 +110,7 @@ void* ctx_pinned(ak_ctx* c, std::size_t bytes);
 std::uint64_t* ctx_split(ak_ctx* c, std::size_t count);
 std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count);
 // MSD-pass tables: [65536 joint counts][65536 16-bit cursors][256 8-bit cursors][8 spare]
+// [64 scan-chunk sums][64 x 256 column partials]
 std::uint64_t* ctx_msd(ak_ctx* c);
 std::uint64_t* ctx_msd3(ak_ctx* c);
 void* ctx_stage(ak_ctx* c, std::size_t bytes);

@@ -7,7 +7,7 @@
 //
 //   hist_joint_kernel: one read of the keys -> the 256-bin histograms of the top three
 //       digits (the plan) and the 65536-bin histogram of the top 16 bits (the cursors);
-//   joint_scan_kernel: exclusive scan of the 65536 counts -> 16-bit bucket starts and the
+//   joint_scan_{a,b}_kernel: exclusive scan of the 65536 counts -> 16-bit bucket starts and the
 //       8-bit bucket starts (the cursors of both passes);
 //   msd_pass_kernel<LEVEL>: LEVEL 1 partitions by the top 8 bits, LEVEL 2 partitions each
 //       top-8 bucket by the next 8 bits (a tile of the LEVEL-1 output spans few top
@@ -108,53 +108,68 @@ __global__ void __launch_bounds__(JH_BLOCK, 1)
     }
 }
 
-// Exclusive scan of the 65536 joint counts (one CTA, warp w owns [2048 w, 2048 w + 2048),
-// coalesced): cur16[b] = start of 16-bit bucket b, cur8[d] = start of 8-bit bucket d; and
-// the digit-7 / digit-6 histograms (rows 7, 6 of g_hist) as the joint's row / column sums.
-__global__ void __launch_bounds__(1024) joint_scan_kernel(const std::uint64_t* __restrict__ g_joint,
-                                                          std::uint64_t* __restrict__ cur16,
-                                                          std::uint64_t* __restrict__ cur8,
-                                                          std::uint64_t* __restrict__ g_hist) {
+// Exclusive scan of the 65536 joint counts in two launches of 64 CTAs (CTA b owns bins
+// [1024 b, 1024 b + 1024) = rows 4b .. 4b+3 of the (digit 7, digit 6) table):
+//   A: CTA-local exclusive scan -> cur16, CTA total -> sums[b], row sums -> digit-7 histogram,
+//      the CTA's column partials -> colpart[b][256];
+//   B: cur16 += sum of the earlier CTAs' totals, cur8 = row starts; CTA 0 folds the column
+//      partials into the digit-6 histogram.
+constexpr int JS_CTAS = JOINT_BINS / 1024;
+__global__ void __launch_bounds__(1024) joint_scan_a_kernel(const std::uint64_t* __restrict__ g_joint,
+                                                            std::uint64_t* __restrict__ cur16,
+                                                            std::uint64_t* __restrict__ sums,
+                                                            std::uint64_t* __restrict__ colpart,
+                                                            std::uint64_t* __restrict__ g_hist) {
     __shared__ std::uint64_t s_w[32];
-    __shared__ std::uint64_t s_col[4][256];
-    constexpr int PER_WARP = JOINT_BINS / 32;  // 2048 = 8 rows of 256
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const std::uint64_t* src = g_joint + w * PER_WARP;
-    std::uint64_t sum = 0;
-    for (int c = 0; c < PER_WARP / 32; ++c) sum += src[c * 32 + lane];
+    const int i = blockIdx.x * 1024 + t;
+    const std::uint64_t v = g_joint[i];
+    std::uint64_t inc = v;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULLM, sum, o);
-    if (lane == 0) s_w[w] = sum;
-    // column sums: thread t adds column t & 255 over rows (t >> 8) * 64 .. + 63
-    {
-        const int col = t & 255, r0 = (t >> 8) * 64;
-        std::uint64_t cs = 0;
-        for (int r = r0; r < r0 + 64; ++r) cs += g_joint[r * 256 + col];
-        s_col[t >> 8][col] = cs;
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    std::uint64_t wp = 0;
+    for (int k = 0; k < w; ++k) wp += s_w[k];
+    cur16[i] = wp + inc - v;
+    if (t == 1023) sums[blockIdx.x] = wp + inc;
+    if ((t & 255) == 255) {  // a row of 256 bins ends here: its sum = prefix difference
+        std::uint64_t row_start = 0;
+        const int r0 = t - 255;  // first bin of the row (block-local)
+        for (int k = 0; k < (r0 >> 5); ++k) row_start += s_w[k];
+        g_hist[7 * 256 + (i >> 8)] += (wp + inc) - row_start;
+    }
+    if (t < 256) {
+        const std::uint64_t* b = g_joint + blockIdx.x * 1024;
+        colpart[blockIdx.x * 256 + t] = b[t] + b[256 + t] + b[512 + t] + b[768 + t];
+    }
+}
+__global__ void __launch_bounds__(1024) joint_scan_b_kernel(std::uint64_t* __restrict__ cur16,
+                                                            std::uint64_t* __restrict__ cur8,
+                                                            const std::uint64_t* __restrict__ sums,
+                                                            const std::uint64_t* __restrict__ colpart,
+                                                            std::uint64_t* __restrict__ g_hist) {
+    __shared__ std::uint64_t s_off;
+    const int t = threadIdx.x;
+    if (t < 32) {
+        std::uint64_t x = 0;
+        for (int k = t; k < static_cast<int>(blockIdx.x); k += 32) x += sums[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLM, x, o);
+        if (t == 0) s_off = x;
     }
     __syncthreads();
-    if (t < 256) g_hist[6 * 256 + t] += s_col[0][t] + s_col[1][t] + s_col[2][t] + s_col[3][t];
-    std::uint64_t carry = 0;
-    for (int i = 0; i < w; ++i) carry += s_w[i];
-    std::uint64_t row = 0;
-    for (int c = 0; c < PER_WARP / 32; ++c) {
-        const int b = w * PER_WARP + c * 32 + lane;
-        const std::uint64_t v = g_joint[b];
-        std::uint64_t inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const std::uint64_t y = __shfl_up_sync(FULLM, inc, o);
-            if (lane >= o) inc += y;
-        }
-        cur16[b] = carry + inc - v;
-        if ((b & 0xff) == 0) cur8[b >> 8] = carry + inc - v;
-        const std::uint64_t tot = __shfl_sync(FULLM, inc, 31);
-        carry += tot;
-        row += tot;
-        if ((c & 7) == 7) {  // a 256-bin row (8 chunks) is complete: digit-7 histogram
-            if (lane == 0) g_hist[7 * 256 + (b >> 8)] += row;
-            row = 0;
-        }
+    const int i = blockIdx.x * 1024 + t;
+    const std::uint64_t c = cur16[i] + s_off;
+    cur16[i] = c;
+    if ((i & 0xff) == 0) cur8[i >> 8] = c;
+    if (blockIdx.x == 0 && t < 256) {
+        std::uint64_t x = 0;
+        for (int k = 0; k < JS_CTAS; ++k) x += colpart[k * 256 + t];
+        g_hist[6 * 256 + t] += x;
     }
 }
 
@@ -459,7 +474,11 @@ void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t
         hist_joint_kernel<T, false><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
-    joint_scan_kernel<<<1, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, g_joint + 2 * JOINT_BINS, g_hist);
+    std::uint64_t* sums = g_joint + 2 * JOINT_BINS + 256 + 8;  // ctx_msd tail
+    std::uint64_t* colpart = sums + JS_CTAS;
+    joint_scan_a_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, sums, colpart, g_hist);
+    joint_scan_b_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint + JOINT_BINS, g_joint + 2 * JOINT_BINS, sums, colpart,
+                                                         g_hist);
     AKB_CUDA(cudaGetLastError());
     c->kernel_launches += 1;
 }
