@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(RED_BLOCK)
 template <typename T>
 struct scan_cfg {
     // 256 threads and 32 KB tiles for every element size (16 x 8 B or 32 x 4 B per thread);
-    // 4 tiles in flight per SM hide the look-back round trips.
+    // 6 tiles in flight per SM (40 registers: runs are re-read from shared memory, not held)
+    // hide the look-back round trips.
     static constexpr int BLOCK = 256;
     static constexpr int ITEMS = 32 / sizeof(T) * 4;
     static constexpr int TILE = BLOCK * ITEMS;
@@ -199,62 +200,33 @@ struct local_acc_of {
     using type = T;
 };
 
-template <typename T, int OP, bool VECIO>
-__global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 4)
-    scan_kernel(const T* x, T* out, std::uint64_t n, T init, int inclusive, std::uint32_t* flags,
-                std::uint64_t* vals, std::uint32_t tag, std::uint32_t* tile_counter) {
+// Scan of one tile already staged in the padded shared tile: thread-serial runs -> warp /
+// block scan -> decoupled look-back -> results written back into the same shared slots.
+// Ends with a __syncthreads (the tile is ready to store).
+template <typename T, int OP>
+__device__ __forceinline__ void scan_tile_core(T* s_tile, typename acc_of<T>::type* s_warp,
+                                               typename acc_of<T>::type& s_excl, std::uint32_t tile,
+                                               std::uint64_t rem, bool full, T init, int inclusive,
+                                               std::uint64_t* vals, std::uint32_t tag) {
     using A = typename acc_of<T>::type;
     using F = opf<A, OP>;
     using LA = typename local_acc_of<T>::type;
     using FL = opf<LA, OP>;
     using Cfg = scan_cfg<T>;
     constexpr int ITEMS = Cfg::ITEMS;
-    constexpr int TILE = Cfg::TILE;
-    constexpr int VEC = Cfg::VEC;
     constexpr int SCAN_BLOCK = Cfg::BLOCK;
     constexpr int WARPS = SCAN_BLOCK / 32;
-    __shared__ __align__(16) T s_tile[Cfg::PADDED];
-    __shared__ A s_warp[WARPS];
-    __shared__ A s_excl;
-    __shared__ std::uint32_t s_tile_id;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile_id = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const std::uint32_t tile = s_tile_id;
-    const std::uint64_t base = static_cast<std::uint64_t>(tile) * TILE;
-    const std::uint64_t rem = n - base;
-    const bool full = rem >= static_cast<std::uint64_t>(TILE);
-
-    // ---- load: global (coalesced) -> padded shared tile ----
-    if (VECIO && full) {
-        const uint4* src = reinterpret_cast<const uint4*>(x + base);
-        uint4 q[TILE / VEC / SCAN_BLOCK];
-#pragma unroll
-        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) q[j] = __ldg(src + j * SCAN_BLOCK + tid);
-#pragma unroll
-        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) {
-            const T* e = reinterpret_cast<const T*>(&q[j]);
-            const int e0 = (j * SCAN_BLOCK + tid) * VEC;
-#pragma unroll
-            for (int k = 0; k < VEC; ++k) s_tile[scan_slot<ITEMS>(e0 + k)] = e[k];
-        }
-    } else {
-#pragma unroll 4
-        for (int e = tid; e < TILE; e += SCAN_BLOCK)
-            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot<ITEMS>(e)] = x[base + e];
-    }
-    __syncthreads();
-
     // ---- thread-serial scan of 16 contiguous elements ----
+    // (pass 1 only totals the run; pass 2 below re-reads it from shared memory and
+    // rebuilds the same prefixes, so no per-item registers live across the look-back)
     const int my0 = tid * ITEMS;
-    LA v[ITEMS];
     LA run = FL::identity();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const bool ok = full || static_cast<std::uint64_t>(my0 + i) < rem;
         const LA xi = ok ? static_cast<LA>(s_tile[scan_slot<ITEMS>(my0 + i)]) : FL::identity();
         run = FL::apply(run, xi);
-        v[i] = run;  // thread-local inclusive prefix
     }
     // warp scan of thread totals
     A winc = static_cast<A>(run);
@@ -336,15 +308,67 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 4)
 
     // ---- results back into this thread's own shared slots ----
     const A pre = F::apply(F::apply(F::apply(static_cast<A>(init), s_excl), wexcl), texcl);
-    if (inclusive) {
+    LA r = FL::identity();
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) s_tile[scan_slot<ITEMS>(my0 + i)] = static_cast<T>(F::apply(pre, static_cast<A>(v[i])));
-    } else {
-        s_tile[scan_slot<ITEMS>(my0)] = static_cast<T>(pre);
-#pragma unroll
-        for (int i = 1; i < ITEMS; ++i) s_tile[scan_slot<ITEMS>(my0 + i)] = static_cast<T>(F::apply(pre, static_cast<A>(v[i - 1])));
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool ok = full || static_cast<std::uint64_t>(my0 + i) < rem;
+        const int slot = scan_slot<ITEMS>(my0 + i);
+        const LA xi = ok ? static_cast<LA>(s_tile[slot]) : FL::identity();
+        const LA before = r;
+        r = FL::apply(r, xi);  // thread-local inclusive prefix, as in pass 1
+        s_tile[slot] = static_cast<T>(F::apply(pre, static_cast<A>(inclusive ? r : before)));
     }
     __syncthreads();
+
+}
+
+template <typename T, int OP, bool VECIO>
+__global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
+    scan_kernel(const T* x, T* out, std::uint64_t n, T init, int inclusive, std::uint32_t* flags,
+                std::uint64_t* vals, std::uint32_t tag, std::uint32_t* tile_counter) {
+    using A = typename acc_of<T>::type;
+    using F = opf<A, OP>;
+    using LA = typename local_acc_of<T>::type;
+    using FL = opf<LA, OP>;
+    using Cfg = scan_cfg<T>;
+    constexpr int ITEMS = Cfg::ITEMS;
+    constexpr int TILE = Cfg::TILE;
+    constexpr int VEC = Cfg::VEC;
+    constexpr int SCAN_BLOCK = Cfg::BLOCK;
+    constexpr int WARPS = SCAN_BLOCK / 32;
+    __shared__ __align__(16) T s_tile[Cfg::PADDED];
+    __shared__ A s_warp[WARPS];
+    __shared__ A s_excl;
+    __shared__ std::uint32_t s_tile_id;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile_id = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const std::uint32_t tile = s_tile_id;
+    const std::uint64_t base = static_cast<std::uint64_t>(tile) * TILE;
+    const std::uint64_t rem = n - base;
+    const bool full = rem >= static_cast<std::uint64_t>(TILE);
+
+    // ---- load: global (coalesced) -> padded shared tile ----
+    if (VECIO && full) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + base);
+        uint4 q[TILE / VEC / SCAN_BLOCK];
+#pragma unroll
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) q[j] = __ldg(src + j * SCAN_BLOCK + tid);
+#pragma unroll
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) {
+            const T* e = reinterpret_cast<const T*>(&q[j]);
+            const int e0 = (j * SCAN_BLOCK + tid) * VEC;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) s_tile[scan_slot<ITEMS>(e0 + k)] = e[k];
+        }
+    } else {
+#pragma unroll 4
+        for (int e = tid; e < TILE; e += SCAN_BLOCK)
+            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot<ITEMS>(e)] = x[base + e];
+    }
+    __syncthreads();
+
+    scan_tile_core<T, OP>(s_tile, s_warp, s_excl, tile, rem, full, init, inclusive, vals, tag);
 
     // ---- store: padded shared tile -> global (coalesced) ----
     if (VECIO && full) {
@@ -410,9 +434,19 @@ void scan(ak_ctx* c, const T* x, T* out, std::uint64_t n, int op, int inclusive,
     AKB_CUDA(cudaMemsetAsync(counter, 0, 4, c->stream));
     const int tok = ctx_prof_begin(c, KF_SCAN);
     const bool vecio = ((reinterpret_cast<std::uintptr_t>(x) | reinterpret_cast<std::uintptr_t>(out)) & 15) == 0;
+    // 6 x 35 KB tiles per SM: ask for the full shared-memory carveout once per instantiation
 #define AKB_SCAN(OPV, V)                                                                       \
-    scan_kernel<T, OPV, V><<<static_cast<unsigned>(tiles), scan_cfg<T>::BLOCK, 0, c->stream>>>(         \
-        x, out, n, init, inclusive, c->scan_flags, c->scan_vals, tag, counter)
+    do {                                                                                       \
+        static bool carve = false;                                                             \
+        if (!carve) {                                                                          \
+            AKB_CUDA(cudaFuncSetAttribute(scan_kernel<T, OPV, V>,                              \
+                                          cudaFuncAttributePreferredSharedMemoryCarveout,      \
+                                          cudaSharedmemCarveoutMaxShared));                    \
+            carve = true;                                                                      \
+        }                                                                                      \
+        scan_kernel<T, OPV, V><<<static_cast<unsigned>(tiles), scan_cfg<T>::BLOCK, 0, c->stream>>>(     \
+            x, out, n, init, inclusive, c->scan_flags, c->scan_vals, tag, counter);            \
+    } while (0)
     if (vecio) {
         if (op == OP_SUM) AKB_SCAN(OP_SUM, true);
         else if (op == OP_MIN) AKB_SCAN(OP_MIN, true);

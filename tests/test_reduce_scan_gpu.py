@@ -103,6 +103,29 @@ def test_accumulate_minmax(ak, ex, dev):
     assert np.array_equal(got, np.minimum.accumulate(x))
 
 
+@pytest.mark.parametrize("dt", [np.int32, np.int64, np.uint64, np.float64])
+@pytest.mark.parametrize("n", [(1 << 23), (1 << 23) + 12345])
+def test_accumulate_persistent_path(ak, orc, ex, dev, dt, n):
+    """Sizes past 4 x SM-count tiles take the persistent TMA-fed scan (scan_persist_kernel):
+    inclusive, exclusive and in-place (x is out) sums, and running max, exact vs the oracle."""
+    x = vals(np.random.default_rng(n + 7), dt, n)
+    for inclusive in (True, False):
+        got = ak.accumulate("sum", t(x, dev), inclusive=inclusive, ex=ex).cpu().numpy()
+        if np.dtype(dt).kind == "f":
+            want = orc.scan(x, inclusive)
+            assert (np.abs(got - want) / np.maximum(1.0, np.abs(want))).max() <= 1e-10
+        elif dt == np.uint64:
+            want = np.cumsum(x, dtype=np.uint64)
+            if not inclusive:
+                want = np.concatenate([[0], want[:-1]]).astype(np.uint64)
+            assert np.array_equal(got, want)
+        else:
+            assert np.array_equal(got, orc.scan(x, inclusive))
+    d = t(x, dev)
+    ak.accumulate("max", d, out=d, init=x.min(), ex=ex)  # in place
+    assert np.array_equal(d.cpu().numpy(), np.maximum.accumulate(x))
+
+
 @pytest.mark.parametrize("n", [10, 100_000, 5_000_000])
 def test_accumulate_f32_tolerance(ak, orc, ex, dev, n):
     x = vals(np.random.default_rng(n), np.float32, n)
