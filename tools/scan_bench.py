@@ -32,8 +32,7 @@ def main():
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     ms = sum(ts) / reps
-    print(f"scan {dt} 2^{n.bit_length() - 1}: {ms:.4f} ms  {2 * n * x.element_size() / ms / 1e6:.1f} GB/s "
-          f"(AKB_SCAN_PERSIST={os.environ.get('AKB_SCAN_PERSIST', '1')})")
+    print(f"scan {dt} 2^{n.bit_length() - 1}: {ms:.4f} ms  {2 * n * x.element_size() / ms / 1e6:.1f} GB/s")
 
 
 if __name__ == "__main__":
