@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(RED_BLOCK)
 // ---------------------------------------------------------------------------
 // K2: single-pass scan, dynamic tiles, decoupled look-back (Merrill & Garland;
 // the "opportunistic look-back" of PAPER.md:161).
-//   load   : coalesced 16-byte loads, transposed through a padded shared tile
-//            (one pad element per 16 -> conflict-free blocked reads);
+//   load   : coalesced 16-byte loads, transposed through a shared tile whose 16-byte
+//            chunks are XOR-swizzled per thread run (conflict-free 16-byte accesses
+//            in both the coalesced and the per-run order);
 //   local  : each thread scans its 16 contiguous elements serially, warp shuffle
 //            scan of thread totals, block scan of 8 warp totals;
 //   chain  : warp 0 publishes the tile aggregate, looks back 32 tiles per round
@@ -179,19 +180,21 @@ __global__ void __launch_bounds__(RED_BLOCK)
 template <typename T>
 struct scan_cfg {
     // 256 threads and 32 KB tiles for every element size (16 x 8 B or 32 x 4 B per thread);
-    // 6 tiles in flight per SM (40 registers: runs are re-read from shared memory, not held)
+    // 6 tiles in flight per SM (runs are re-read from shared memory, not held in registers)
     // hide the look-back round trips.
     static constexpr int BLOCK = 256;
     static constexpr int ITEMS = 32 / sizeof(T) * 4;
     static constexpr int TILE = BLOCK * ITEMS;
-    static constexpr int PADDED = TILE + TILE / ITEMS;  // one pad slot per thread run
     static constexpr int VEC = 16 / sizeof(T);
+    static constexpr int CHUNKS = ITEMS / VEC;  // 16-byte chunks per thread run (8)
 };
 
-// element e of the tile lives at e + e / ITEMS: each thread's run of ITEMS contiguous
-// elements starts on a different bank (conflict-free blocked reads and writes)
-template <int ITEMS>
-__device__ __forceinline__ int scan_slot(int e) { return e + e / ITEMS; }
+// 16-byte chunk g of the tile (thread run t = g / 8, chunk j = g % 8 of the run) lives at
+// chunk t * 8 + (j ^ (t & 7)): eight consecutive threads reading chunk j of their runs hit
+// eight different 16-byte bank groups, and so do eight consecutive coalesced chunks.
+__device__ __forceinline__ int scan_chunk(int g) { return (g & ~7) | ((g ^ (g >> 3)) & 7); }
+template <int VEC>
+__device__ __forceinline__ int scan_slot(int e) { return scan_chunk(e / VEC) * VEC + e % VEC; }
 
 // In-thread accumulation type: floats scan their 32-element run in float (error ~1e-7 of
 // the run) and carry everything beyond the run in double (acc_of).
@@ -220,13 +223,21 @@ __device__ __forceinline__ void scan_tile_core(T* s_tile, typename acc_of<T>::ty
     // ---- thread-serial scan of 16 contiguous elements ----
     // (pass 1 only totals the run; pass 2 below re-reads it from shared memory and
     // rebuilds the same prefixes, so no per-item registers live across the look-back)
+    constexpr int VEC = Cfg::VEC;
+    constexpr int CHUNKS = Cfg::CHUNKS;
+    static_assert(CHUNKS == 8, "the chunk swizzle assumes 8 chunks per thread run");
+    uint4* s4 = reinterpret_cast<uint4*>(s_tile);
     const int my0 = tid * ITEMS;
     LA run = FL::identity();
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const bool ok = full || static_cast<std::uint64_t>(my0 + i) < rem;
-        const LA xi = ok ? static_cast<LA>(s_tile[scan_slot<ITEMS>(my0 + i)]) : FL::identity();
-        run = FL::apply(run, xi);
+    for (int j = 0; j < CHUNKS; ++j) {
+        const uint4 q = s4[tid * CHUNKS + (j ^ (tid & 7))];
+        const T* e = reinterpret_cast<const T*>(&q);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            const bool ok = full || static_cast<std::uint64_t>(my0 + j * VEC + k) < rem;
+            run = FL::apply(run, ok ? static_cast<LA>(e[k]) : FL::identity());
+        }
     }
     // warp scan of thread totals
     A winc = static_cast<A>(run);
@@ -310,13 +321,18 @@ __device__ __forceinline__ void scan_tile_core(T* s_tile, typename acc_of<T>::ty
     const A pre = F::apply(F::apply(F::apply(static_cast<A>(init), s_excl), wexcl), texcl);
     LA r = FL::identity();
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const bool ok = full || static_cast<std::uint64_t>(my0 + i) < rem;
-        const int slot = scan_slot<ITEMS>(my0 + i);
-        const LA xi = ok ? static_cast<LA>(s_tile[slot]) : FL::identity();
-        const LA before = r;
-        r = FL::apply(r, xi);  // thread-local inclusive prefix, as in pass 1
-        s_tile[slot] = static_cast<T>(F::apply(pre, static_cast<A>(inclusive ? r : before)));
+    for (int j = 0; j < CHUNKS; ++j) {
+        uint4& qr = s4[tid * CHUNKS + (j ^ (tid & 7))];
+        uint4 q = qr;
+        T* e = reinterpret_cast<T*>(&q);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            const bool ok = full || static_cast<std::uint64_t>(my0 + j * VEC + k) < rem;
+            const LA before = r;
+            r = FL::apply(r, ok ? static_cast<LA>(e[k]) : FL::identity());  // as in pass 1
+            e[k] = static_cast<T>(F::apply(pre, static_cast<A>(inclusive ? r : before)));
+        }
+        qr = q;
     }
     __syncthreads();
 
@@ -331,12 +347,11 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
     using LA = typename local_acc_of<T>::type;
     using FL = opf<LA, OP>;
     using Cfg = scan_cfg<T>;
-    constexpr int ITEMS = Cfg::ITEMS;
     constexpr int TILE = Cfg::TILE;
     constexpr int VEC = Cfg::VEC;
     constexpr int SCAN_BLOCK = Cfg::BLOCK;
     constexpr int WARPS = SCAN_BLOCK / 32;
-    __shared__ __align__(16) T s_tile[Cfg::PADDED];
+    __shared__ __align__(16) T s_tile[TILE];
     __shared__ A s_warp[WARPS];
     __shared__ A s_excl;
     __shared__ std::uint32_t s_tile_id;
@@ -355,16 +370,12 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
 #pragma unroll
         for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) q[j] = __ldg(src + j * SCAN_BLOCK + tid);
 #pragma unroll
-        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) {
-            const T* e = reinterpret_cast<const T*>(&q[j]);
-            const int e0 = (j * SCAN_BLOCK + tid) * VEC;
-#pragma unroll
-            for (int k = 0; k < VEC; ++k) s_tile[scan_slot<ITEMS>(e0 + k)] = e[k];
-        }
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j)
+            reinterpret_cast<uint4*>(s_tile)[scan_chunk(j * SCAN_BLOCK + tid)] = q[j];
     } else {
 #pragma unroll 4
         for (int e = tid; e < TILE; e += SCAN_BLOCK)
-            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot<ITEMS>(e)] = x[base + e];
+            if (static_cast<std::uint64_t>(e) < rem) s_tile[scan_slot<VEC>(e)] = x[base + e];
     }
     __syncthreads();
 
@@ -374,18 +385,12 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
     if (VECIO && full) {
         uint4* dst = reinterpret_cast<uint4*>(out + base);
 #pragma unroll
-        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j) {
-            uint4 q;
-            T* e = reinterpret_cast<T*>(&q);
-            const int e0 = (j * SCAN_BLOCK + tid) * VEC;
-#pragma unroll
-            for (int k = 0; k < VEC; ++k) e[k] = s_tile[scan_slot<ITEMS>(e0 + k)];
-            dst[j * SCAN_BLOCK + tid] = q;
-        }
+        for (int j = 0; j < TILE / VEC / SCAN_BLOCK; ++j)
+            dst[j * SCAN_BLOCK + tid] = reinterpret_cast<const uint4*>(s_tile)[scan_chunk(j * SCAN_BLOCK + tid)];
     } else {
 #pragma unroll 4
         for (int e = tid; e < TILE; e += SCAN_BLOCK)
-            if (static_cast<std::uint64_t>(e) < rem) out[base + e] = s_tile[scan_slot<ITEMS>(e)];
+            if (static_cast<std::uint64_t>(e) < rem) out[base + e] = s_tile[scan_slot<VEC>(e)];
     }
 }
 
@@ -434,7 +439,7 @@ void scan(ak_ctx* c, const T* x, T* out, std::uint64_t n, int op, int inclusive,
     AKB_CUDA(cudaMemsetAsync(counter, 0, 4, c->stream));
     const int tok = ctx_prof_begin(c, KF_SCAN);
     const bool vecio = ((reinterpret_cast<std::uintptr_t>(x) | reinterpret_cast<std::uintptr_t>(out)) & 15) == 0;
-    // 6 x 35 KB tiles per SM: ask for the full shared-memory carveout once per instantiation
+    // 6 x 32 KB tiles per SM: ask for the full shared-memory carveout once per instantiation
 #define AKB_SCAN(OPV, V)                                                                       \
     do {                                                                                       \
         static bool carve = false;                                                             \
