@@ -1831,6 +1831,11 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         // the MSD cursors end at the bucket ends: cuts[j] = end of bucket j - 1 (no search)
         cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(msdbuf + 65536, J, n,
                                                                                                  cuts);
+    else if (bucket_mode && !used_msd && m == 1 && J == RADIX)
+        // one onesweep pass over digit top - 1: bucket j starts at that digit's exclusive
+        // global offset j (hist_scan_kernel), so cuts[j] = offs[j] (no search)
+        cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
+            g_offs + (top - 1) * RADIX + 1, J, n, cuts);
     else if (bucket_mode)
         bucket_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
             G, n, top_shift, desc ? 1 : 0, J, base_id, cuts);
