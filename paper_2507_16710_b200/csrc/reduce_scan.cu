@@ -203,7 +203,7 @@ struct local_acc_of {
     using type = T;
 };
 
-// Scan of one tile already staged in the padded shared tile: thread-serial runs -> warp /
+// Scan of one tile already staged in the swizzled shared tile: thread-serial runs -> warp /
 // block scan -> decoupled look-back -> results written back into the same shared slots.
 // Ends with a __syncthreads (the tile is ready to store).
 template <typename T, int OP>
@@ -220,7 +220,7 @@ __device__ __forceinline__ void scan_tile_core(T* s_tile, typename acc_of<T>::ty
     constexpr int SCAN_BLOCK = Cfg::BLOCK;
     constexpr int WARPS = SCAN_BLOCK / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // ---- thread-serial scan of 16 contiguous elements ----
+    // ---- thread-serial scan of ITEMS contiguous elements (16 x 8 B or 32 x 4 B) ----
     // (pass 1 only totals the run; pass 2 below re-reads it from shared memory and
     // rebuilds the same prefixes, so no per-item registers live across the look-back)
     constexpr int VEC = Cfg::VEC;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
     const std::uint64_t rem = n - base;
     const bool full = rem >= static_cast<std::uint64_t>(TILE);
 
-    // ---- load: global (coalesced) -> padded shared tile ----
+    // ---- load: global (coalesced) -> swizzled shared tile ----
     if (VECIO && full) {
         const uint4* src = reinterpret_cast<const uint4*>(x + base);
         uint4 q[TILE / VEC / SCAN_BLOCK];
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
 
     scan_tile_core<T, OP>(s_tile, s_warp, s_excl, tile, rem, full, init, inclusive, vals, tag);
 
-    // ---- store: padded shared tile -> global (coalesced) ----
+    // ---- store: swizzled shared tile -> global (coalesced) ----
     if (VECIO && full) {
         uint4* dst = reinterpret_cast<uint4*>(out + base);
 #pragma unroll
