@@ -14,8 +14,10 @@
 #pragma once
 
 #include <cstddef>
+#include <algorithm>
 #include <cstdint>
 #include <span>
+#include <stdexcept>
 #include <type_traits>
 #include <utility>
 #include <vector>
@@ -49,7 +51,70 @@ struct sih_stats {
 /// The library's device sorter, usable in the Sorter slot.
 struct cuda_sorter {};
 
+/// sihsort.hpp:28-34: equal-width histogram over the sampled key range (long double edges).
+struct key_histogram {
+    std::vector<long double> bin_edges;  // K+1 (single bin when degenerate)
+    std::vector<std::uint64_t> counts;   // K
+    std::uint64_t total = 0;
+};
+
+/// sihsort.hpp:36-42: P-1 nondecreasing splitters; keys equal to a splitter go to the lower rank.
+template <typename T>
+struct splitter_set {
+    std::vector<T> values;
+};
+
+/// sihsort.hpp:351-357.
+template <typename T>
+struct refine_result {
+    splitter_set<T> splitters;
+    std::size_t rounds_used = 0;
+    bool converged = false;
+    double max_deviation = 0.0;
+};
+
 namespace detail {
+
+#define AK_STAGE_DISPATCH(S, T)                                                                                  \
+    inline int c_sample_local(ak_ctx* c, const T* d, std::uint64_t n, std::uint64_t k, T* h, std::uint64_t* cnt) {  \
+        return ak_sample_local_##S(c, d, n, k, h, cnt);                                                          \
+    }                                                                                                            \
+    inline int c_histogram(const T* smp, std::uint64_t m, std::uint64_t bins, long double* e, std::uint64_t* cts,    \
+                           std::uint64_t cap, std::uint64_t* nb, std::uint64_t* tot) {                            \
+        return ak_build_interpolated_histogram_##S(smp, m, bins, e, cts, cap, nb, tot);                          \
+    }                                                                                                            \
+    inline int c_select(const long double* e, const std::uint64_t* cts, std::uint64_t nb, std::uint64_t tot,       \
+                        std::uint64_t world, T* out) {                                                           \
+        return ak_select_splitters_##S(e, cts, nb, tot, world, out);                                             \
+    }                                                                                                            \
+    inline int c_refine(ak_ctx* c, ak_comm* cm, const T* d, std::uint64_t n, T* spl, std::uint64_t m,              \
+                        const ak_sih_config* cfg, std::uint64_t* rounds, int* conv, double* dev) {               \
+        return ak_refine_splitters_##S(c, cm, d, n, spl, m, cfg, rounds, conv, dev);                             \
+    }                                                                                                            \
+    inline int c_redistribute(ak_ctx* c, ak_comm* cm, const T* d, std::uint64_t n, const T* spl, std::uint64_t m,  \
+                              std::uint64_t nt, T* out, std::uint64_t cap, std::uint64_t* oc) {                  \
+        return ak_redistribute_##S(c, cm, d, n, spl, m, nt, out, cap, oc, nullptr, nullptr);                     \
+    }
+AK_STAGE_DISPATCH(i32, std::int32_t)
+AK_STAGE_DISPATCH(u32, std::uint32_t)
+AK_STAGE_DISPATCH(i64, std::int64_t)
+AK_STAGE_DISPATCH(u64, std::uint64_t)
+AK_STAGE_DISPATCH(f32, float)
+AK_STAGE_DISPATCH(f64, double)
+#undef AK_STAGE_DISPATCH
+
+/// A span's keys in HBM: the span itself when it is device memory, else a staged copy.
+template <typename T>
+struct device_view {
+    device_buffer<T> staged;
+    const T* p;
+    device_view(ak_ctx* c, std::span<const T> s) : staged(c, on_device(s.data()) ? 0 : s.size()), p(s.data()) {
+        if (!on_device(s.data())) {
+            staged.upload(s.data(), s.size());
+            p = staged.p;
+        }
+    }
+};
 
 #define AK_SIH_DISPATCH(S, T)                                                                                 \
     inline int c_sihsort_host(ak_ctx* c, ak_comm* cm, const T* in, std::uint64_t n, T* out, std::uint64_t cap, \
@@ -121,6 +186,102 @@ std::pair<std::vector<T>, sih_stats> sihsort(std::vector<T> local_data, Comm& co
     static_assert(std::is_same_v<std::remove_cvref_t<Sorter>, cuda_sorter>,
                   "ak (B200 build): the local sorter runs on the device; pass ak::cuda_sorter{}");
     return sihsort<T>(std::move(local_data), comm, cfg, ex);
+}
+
+// ---- stage functions (sihsort.hpp:264-501); sorted spans may be host or device memory ----
+
+/// k evenly spaced order statistics of a sorted local array (sihsort.hpp:264-282): positions
+/// round-half-up(j(n-1)/(k-1)), k = 1 probes n/2, k clamps to n; gathered on the device.
+template <typename T>
+std::vector<T> sample_local(std::span<const T> sorted_local, std::size_t k,
+                            const exec_backend& ex = detail::default_backend()) {
+    detail::require_key<T>();
+    const std::size_t n = sorted_local.size();
+    if (n == 0 || k == 0) return {};
+    std::vector<T> out(std::min(k, n));
+    detail::device_view<T> d(ex.ctx(), sorted_local);
+    std::uint64_t cnt = 0;
+    detail::check(detail::c_sample_local(ex.ctx(), d.p, n, k, out.data(), &cnt));
+    out.resize(cnt);
+    return out;
+}
+
+/// Equal-width histogram of gathered samples over [min, max] (sihsort.hpp:286-305); host math
+/// in long double, as the reference (tiny, parity-critical).
+template <typename T>
+key_histogram build_interpolated_histogram(std::span<const T> all_samples, std::size_t bins) {
+    detail::require_key<T>();
+    const std::size_t cap = bins > 0 ? bins : 1;
+    key_histogram h;
+    h.bin_edges.resize(cap + 1);
+    h.counts.resize(cap);
+    std::uint64_t nb = 0, tot = 0;
+    detail::check(detail::c_histogram(all_samples.data(), all_samples.size(), bins, h.bin_edges.data(),
+                                      h.counts.data(), cap, &nb, &tot));
+    h.bin_edges.resize(nb + 1);
+    h.counts.resize(nb);
+    h.total = tot;
+    return h;
+}
+
+/// P-1 splitters at the estimated global quantiles (sihsort.hpp:310-349).
+template <typename T>
+splitter_set<T> select_splitters(const key_histogram& hist, std::size_t world) {
+    detail::require_key<T>();
+    splitter_set<T> out;
+    if (world <= 1) return out;
+    if (hist.counts.empty() || hist.bin_edges.size() != hist.counts.size() + 1)
+        throw std::invalid_argument("select_splitters: malformed histogram");
+    out.values.resize(world - 1);
+    detail::check(detail::c_select(hist.bin_edges.data(), hist.counts.data(), hist.counts.size(), hist.total, world,
+                                   out.values.data()));
+    return out;
+}
+
+/// Exact-count splitter refinement (sihsort.hpp:364-464). Collective over comm.
+template <typename T, typename Comm>
+refine_result<T> refine_splitters(std::span<const T> local_sorted, splitter_set<T> splitters, Comm& comm,
+                                  const sih_config& cfg, const exec_backend& ex = detail::default_backend()) {
+    detail::require_key<T>();
+    const ak_sih_config c = detail::to_c(cfg);
+    detail::device_view<T> d(ex.ctx(), local_sorted);
+    refine_result<T> r;
+    std::uint64_t rounds = 0;
+    int conv = 0;
+    double dev = 0.0;
+    detail::check(detail::c_refine(ex.ctx(), comm.handle(), d.p, local_sorted.size(), splitters.values.data(),
+                                   splitters.values.size(), &c, &rounds, &conv, &dev));
+    r.splitters = std::move(splitters);
+    r.rounds_used = rounds;
+    r.converged = conv != 0;
+    r.max_deviation = dev;
+    return r;
+}
+
+/// One all-to-all pass (sihsort.hpp:472-501): the received slices plus the kept local slice,
+/// concatenated in SOURCE-RANK order (not merged). n_total = the agreed global count (it only
+/// fixes the reference's piggyback accounting here; sizes travel in a count exchange).
+template <typename T, typename Comm>
+std::vector<T> redistribute(std::span<const T> local_sorted, const splitter_set<T>& splitters, Comm& comm,
+                            std::uint64_t n_total, const exec_backend& ex = detail::default_backend()) {
+    detail::require_key<T>();
+    detail::device_view<T> d(ex.ctx(), local_sorted);
+    std::uint64_t cap = local_sorted.size() + local_sorted.size() / 4 + 4096;
+    for (;;) {
+        detail::device_buffer<T> out(ex.ctx(), cap);
+        std::uint64_t count = 0;
+        const int rc = detail::c_redistribute(ex.ctx(), comm.handle(), d.p, local_sorted.size(),
+                                              splitters.values.data(), splitters.values.size(), n_total, out.p, cap,
+                                              &count);
+        if (rc == AK_ECAPACITY) {  // every rank retries together
+            cap = (count > cap ? count : cap) + cap / 8 + 4096;
+            continue;
+        }
+        detail::check(rc, count);
+        std::vector<T> h(count);
+        out.download(h.data(), count);
+        return h;
+    }
 }
 
 /// Device-resident variant: input stays in HBM, output written to a caller device buffer of

@@ -12,9 +12,13 @@
 #include <array>
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
 #include <exception>
 #include <mutex>
+#include <span>
+#include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "ak/exec.hpp"
@@ -23,14 +27,116 @@ namespace ak {
 
 namespace sim {
 
-/// P logical ranks on one device (sim_comm.hpp:45-80). queue_capacity is accepted for
-/// source compatibility; the device exchange needs no bounded FIFO.
+/// payload: bulk redistribution traffic; control: everything else (sim_comm.hpp:28-31).
+enum class traffic_class { control, payload };
+
+/// sim_comm.hpp:33-39. On the B200 build collective_sends counts the messages this rank
+/// would send in the reference's binomial reduce + broadcast tree (the device transports
+/// gather instead), and control_bytes_peak covers user control-class messages (loopback world).
+struct rank_counters {
+    std::uint64_t p2p_sends = 0;
+    std::uint64_t p2p_bytes = 0;
+    std::uint64_t collective_ops = 0;
+    std::uint64_t collective_sends = 0;
+    std::uint64_t control_bytes_peak = 0;
+};
+
+}  // namespace sim
+
+namespace detail {
+
+/// rank_comm's messaging / collective methods (sim_comm.hpp:84-181) over any ak_comm.
+template <typename Derived>
+class comm_ops {
+public:
+    /// point-to-point message (sim_comm.hpp:92-94)
+    void send(std::size_t dest, std::span<const std::byte> bytes, sim::traffic_class cls = sim::traffic_class::payload,
+              const exec_backend& ex = default_backend()) {
+        check(ak_comm_send(h(), ex.ctx(), static_cast<int>(dest), bytes.data(), bytes.size(),
+                           cls == sim::traffic_class::control ? 1 : 0));
+    }
+    /// next message from src, FIFO per pair (sim_comm.hpp:95-96)
+    std::vector<std::byte> recv(std::size_t src, const exec_backend& ex = default_backend()) {
+        std::vector<std::byte> out(256);
+        for (;;) {
+            std::uint64_t n = 0;
+            const int rc = ak_comm_recv(h(), ex.ctx(), static_cast<int>(src), out.data(), out.size(), &n);
+            if (rc == AK_ECAPACITY) {  // the message stays pending: retry with room
+                out.resize(n);
+                continue;
+            }
+            check(rc, n);
+            out.resize(n);
+            return out;
+        }
+    }
+    template <typename T>
+    void send_values(std::size_t dest, std::span<const T> values, sim::traffic_class cls = sim::traffic_class::payload,
+                     const exec_backend& ex = default_backend()) {
+        static_assert(std::is_trivially_copyable_v<T>);
+        send(dest, std::as_bytes(values), cls, ex);
+    }
+    template <typename T>
+    std::vector<T> recv_values(std::size_t src, const exec_backend& ex = default_backend()) {
+        static_assert(std::is_trivially_copyable_v<T>);
+        const auto bytes = recv(src, ex);
+        if (bytes.size() % sizeof(T) != 0)  // sim_comm.hpp:108-112
+            throw sim::transport_error("recv_values: message size " + std::to_string(bytes.size()) +
+                                       " is not a multiple of the element size (pair " + std::to_string(src) +
+                                       " -> " + std::to_string(static_cast<const Derived*>(this)->rank()) + ")");
+        std::vector<T> out(bytes.size() / sizeof(T));
+        if (!bytes.empty()) std::memcpy(out.data(), bytes.data(), bytes.size());
+        return out;
+    }
+    /// all_reduce of equal-length vectors (sim_comm.hpp:124-149): the vectors are gathered and
+    /// folded in the reference's binomial-tree order (reduce to rank 0 by halving distances),
+    /// so any merge -- commutative or not -- gives the reference's result on every rank.
+    template <typename T, typename Merge>
+    std::vector<T> all_reduce(std::vector<T> local, Merge merge, const exec_backend& ex = default_backend()) {
+        static_assert(std::is_trivially_copyable_v<T>);
+        const std::size_t p = static_cast<const Derived*>(this)->world_size();
+        const std::size_t len = local.size();
+        std::vector<T> all(len * p);
+        // one gather; the loopback world rejects unequal lengths with sim::protocol_error
+        // (sim_comm.hpp:171-176), NCCL ranks must agree on the length as the reference requires
+        check(ak_comm_allgather(h(), ex.ctx(), local.data(), len * sizeof(T), all.data()));
+        std::vector<std::vector<T>> acc(p);
+        for (std::size_t q = 0; q < p; ++q) acc[q].assign(all.begin() + q * len, all.begin() + (q + 1) * len);
+        std::size_t m = 1;
+        while (m * 2 < p) m *= 2;
+        for (; m >= 1; m >>= 1)
+            for (std::size_t r = 0; r < m && r + m < p; ++r) merge(acc[r], acc[r + m]);
+        return acc[0];
+    }
+    template <typename T>
+    std::vector<T> all_reduce_sum(std::vector<T> local, const exec_backend& ex = default_backend()) {
+        return all_reduce(std::move(local),
+                          [](std::vector<T>& a, const std::vector<T>& b) {
+                              for (std::size_t i = 0; i < a.size(); ++i) a[i] += b[i];
+                          },
+                          ex);
+    }
+    sim::rank_counters counters() const {
+        ak_rank_counters c{};
+        check(ak_comm_counters(h(), &c));
+        return {c.p2p_sends, c.p2p_bytes, c.collective_ops, c.collective_sends, c.control_bytes_peak};
+    }
+
+private:
+    ak_comm* h() const { return static_cast<const Derived*>(this)->handle(); }
+};
+
+}  // namespace detail
+
+namespace sim {
+
+/// P logical ranks on one device (sim_comm.hpp:45-80); queue_capacity bounds each ordered
+/// pair's FIFO of user messages (send blocks while it is full). The sihsort exchange moves
+/// device slices directly and needs no FIFO.
 class world {
 public:
     explicit world(std::size_t ranks, std::size_t queue_capacity = 64) {
-        (void)queue_capacity;
-        if (ranks == 0) throw std::invalid_argument("world: rank count must be >= 1");
-        detail::check(ak_world_create(static_cast<int>(ranks), &w_));
+        detail::check(ak_world_create_ex(static_cast<int>(ranks), queue_capacity, &w_));
     }
     world(const world&) = delete;
     world& operator=(const world&) = delete;
@@ -46,7 +152,7 @@ private:
 };
 
 /// Per-rank handle (sim_comm.hpp:84-181); used by one thread.
-class rank_comm {
+class rank_comm : public detail::comm_ops<rank_comm> {
 public:
     rank_comm(world& w, std::size_t rank) { detail::check(ak_comm_loopback_create(w.handle(), static_cast<int>(rank), &c_)); }
     rank_comm(const rank_comm&) = delete;
@@ -56,12 +162,6 @@ public:
     }
     std::size_t rank() const noexcept { return static_cast<std::size_t>(ak_comm_rank(c_)); }
     std::size_t world_size() const noexcept { return static_cast<std::size_t>(ak_comm_size(c_)); }
-    /// all_reduce_sum of a u64 vector (sim_comm.hpp:151-156).
-    std::vector<std::uint64_t> all_reduce_sum(std::vector<std::uint64_t> v,
-                                              const exec_backend& ex = detail::default_backend()) {
-        detail::check(ak_comm_allreduce_sum_u64(c_, ex.ctx(), v.data(), v.size()));
-        return v;
-    }
     ak_comm* handle() const noexcept { return c_; }
 
 private:
@@ -107,8 +207,9 @@ inline unique_id make_unique_id() {
     return id;
 }
 
-/// One GPU's rank of an NCCL world (replaces sim::rank_comm across GPUs).
-class rank_comm {
+/// One GPU's rank of an NCCL world (replaces sim::rank_comm across GPUs). send / recv are
+/// rendezvous (a send returns once the peer has received).
+class rank_comm : public detail::comm_ops<rank_comm> {
 public:
     rank_comm(const unique_id& id, std::size_t nranks, std::size_t rank, int device) {
         detail::check(ak_comm_nccl_create(id.data(), static_cast<int>(nranks), static_cast<int>(rank), device, &c_));
@@ -120,11 +221,6 @@ public:
     }
     std::size_t rank() const noexcept { return static_cast<std::size_t>(ak_comm_rank(c_)); }
     std::size_t world_size() const noexcept { return static_cast<std::size_t>(ak_comm_size(c_)); }
-    std::vector<std::uint64_t> all_reduce_sum(std::vector<std::uint64_t> v,
-                                              const exec_backend& ex = detail::default_backend()) {
-        detail::check(ak_comm_allreduce_sum_u64(c_, ex.ctx(), v.data(), v.size()));
-        return v;
-    }
     ak_comm* handle() const noexcept { return c_; }
 
 private:

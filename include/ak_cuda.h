@@ -149,7 +149,29 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int key_bytes);
     /* P logical ranks on ONE device (sim::world + run_ranks, sim_comm.hpp:41-218) */           \
     int ak_sihsort_loopback_##S(int device, uint64_t P, const T* const* in, const uint64_t* n,  \
                                 T* const* out, const uint64_t* out_cap, uint64_t* out_count,    \
-                                const ak_sih_config* cfg, ak_sih_stats* stats);
+                                const ak_sih_config* cfg, ak_sih_stats* stats);                 \
+    /* sihsort stages. sample_local (sihsort.hpp:264-282): k order statistics of the sorted */  \
+    /* device keys -> host_out[min(k, n)] */                                                    \
+    int ak_sample_local_##S(ak_ctx* ctx, const T* sorted, uint64_t n, uint64_t k, T* host_out,   \
+                            uint64_t* count);                                                   \
+    /* build_interpolated_histogram (sihsort.hpp:286-305) of host samples: edges[nbins + 1], */ \
+    /* counts[nbins], nbins <= max(bins, 1) <= cap_bins */                                       \
+    int ak_build_interpolated_histogram_##S(const T* samples, uint64_t m, uint64_t bins,         \
+                                            long double* edges, uint64_t* counts,               \
+                                            uint64_t cap_bins, uint64_t* nbins, uint64_t* total); \
+    /* select_splitters (sihsort.hpp:310-349) -> out[world - 1] */                              \
+    int ak_select_splitters_##S(const long double* edges, const uint64_t* counts, uint64_t nbins, \
+                                uint64_t total, uint64_t world, T* out);                        \
+    /* refine_splitters (sihsort.hpp:364-464), collective: host splitters[m] refined in place */ \
+    int ak_refine_splitters_##S(ak_ctx* ctx, ak_comm* comm, const T* sorted, uint64_t n,         \
+                                T* splitters, uint64_t m, const ak_sih_config* cfg,             \
+                                uint64_t* rounds_used, int* converged, double* max_deviation);  \
+    /* redistribute (sihsort.hpp:472-501), collective: out (device, capacity cap) = the P */     \
+    /* received slices concatenated in source-rank order (own slice included); sends/bytes */   \
+    /* = the reference's message accounting (may be NULL) */                                    \
+    int ak_redistribute_##S(ak_ctx* ctx, ak_comm* comm, const T* sorted, uint64_t n,             \
+                            const T* splitters, uint64_t m, uint64_t n_total, T* out,           \
+                            uint64_t cap, uint64_t* out_count, uint64_t* sends, uint64_t* bytes);
 
 /* int16 and int128 keys (dtype.hpp:14-21): the sort family only (merge_sort, by_key,
  * sortperm, sortperm_lowmem); int16 sorts widened to int32, int128 as a stable LSD over its
@@ -229,11 +251,34 @@ typedef int (*ak_exchange_fn)(void* user, const void* send_base, const uint64_t*
                               const uint64_t* recv_cnt, uint64_t elem_bytes);
 int ak_comm_callbacks_create(int nranks, int rank, void* user, ak_allgather_fn ag,
                              ak_allreduce_u64_fn ar, ak_exchange_fn ex, ak_comm** out);
+/* one process per GPU, bulk slices moved by a peer-store kernel straight into the peers'
+ * receive buffers (CUDA IPC mappings, P2P over NVLink/NVSwitch; same-GPU processes work too);
+ * tiny control messages through the caller's allgather / allreduce callbacks (e.g. gloo).
+ * Replaces sim_comm's send/recv of redistribute (sihsort.hpp:481-499, sim_comm.cpp:42-90). */
+int ak_comm_ipc_create(int nranks, int rank, int device, void* user, ak_allgather_fn ag,
+                       ak_allreduce_u64_fn ar, ak_comm** out);
+/* bulk payload bytes this rank pushed to peers so far (NCCL / IPC transports; else 0) */
+int ak_comm_bytes_sent(const ak_comm* comm, uint64_t* out);
 /* sim::world + rank_comm (sim_comm.hpp:41-181) on ONE device: P logical ranks, each driven
  * by its own host thread and ak_ctx; collectives are host-level, slices move device to
  * device. abort() wakes every blocked rank with AK_ETRANSPORT (sim_comm.cpp:19-25). */
 typedef struct ak_world ak_world;
 int ak_world_create(int ranks, ak_world** out);
+int ak_world_create_ex(int ranks, uint64_t queue_capacity, ak_world** out); /* sim_comm.hpp:45-47 */
+/* rank_comm::send / recv (sim_comm.hpp:92-96): host bytes, FIFO per ordered pair. Loopback:
+ * bounded queue (send blocks while queue_capacity messages wait); NCCL: rendezvous (returns
+ * once the peer received). recv: if *n (the message size) exceeds cap, AK_ECAPACITY and the
+ * message stays pending for the next recv from src. control: traffic_class::control. */
+int ak_comm_send(ak_comm* comm, ak_ctx* ctx, int dest, const void* bytes, uint64_t n, int control);
+int ak_comm_recv(ak_comm* comm, ak_ctx* ctx, int src, void* buf, uint64_t cap, uint64_t* n);
+/* every rank's `bytes` (same on all ranks), gathered in rank order into out[P * bytes]; counted
+ * as one collective (the basis of rank_comm::all_reduce(local, merge), sim_comm.hpp:124-149) */
+int ak_comm_allgather(ak_comm* comm, ak_ctx* ctx, const void* in, uint64_t bytes, void* out);
+/* rank_counters (sim_comm.hpp:33-39) */
+typedef struct ak_rank_counters {
+    uint64_t p2p_sends, p2p_bytes, collective_ops, collective_sends, control_bytes_peak;
+} ak_rank_counters;
+int ak_comm_counters(const ak_comm* comm, ak_rank_counters* out);
 int ak_world_size(const ak_world* w);
 int ak_world_abort(ak_world* w);
 int ak_world_destroy(ak_world* w);

@@ -300,6 +300,19 @@ def ref_sihsort(inputs, cfg: SihConfig | None = None, threads_per_rank: int = 0)
     return outs, stats
 
 
+def ref_bench_keys(seed: int, rank: int, n: int, dtype=np.int64, out: np.ndarray | None = None) -> np.ndarray:
+    """Per-rank inputs of the reference bench (bench.cpp:44-62, :164-173) made inside oracle/_ref,
+    so a process timing the reference never loads the product library."""
+    dt = np.dtype(dtype)
+    if out is None:
+        out = np.empty(n, dtype=dt)
+    fn = getattr(ref(), "ref_bench_keys_" + SUFFIX[dt])
+    fn.argtypes = [_u64, _u64, _u64, _p]
+    if fn(seed, rank, n, _ptr(out)) != 0:
+        raise RuntimeError("ref bench_keys")
+    return out
+
+
 def ref_sortperm_bytes(n: int, key_bytes: int, index_bytes: int, lowmem: bool) -> int:
     fn = ref().ref_sortperm_bytes
     fn.restype = _u64

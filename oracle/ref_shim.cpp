@@ -14,6 +14,8 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <random>
+#include <type_traits>
 #include <span>
 #include <vector>
 
@@ -253,6 +255,30 @@ REF_SIH(i64, std::int64_t)
 REF_SIH(u64, std::uint64_t)
 REF_SIH(f32, float)
 REF_SIH(f64, double)
+
+// ---- reference bench inputs (bench.cpp:44-62 random_keys, :164-173 generate_rank_inputs;
+// both sit in an anonymous namespace of src/bench.cpp, so they are restated here) ----
+// Lets the reference arm of bench.py make its inputs without loading the product library.
+template <typename T>
+void bench_keys_impl(std::uint64_t seed, std::uint64_t rank, std::uint64_t n, T* out) {
+    std::mt19937_64 rng(seed + 0x9e3779b97f4a7c15ULL * (rank + 1));  // bench.cpp:168
+    if constexpr (std::is_integral_v<T>) {
+        for (std::uint64_t i = 0; i < n; ++i) out[i] = static_cast<T>(rng());  // bench.cpp:50-52
+    } else {
+        std::uniform_real_distribution<T> dist(T(-1e6), T(1e6));  // bench.cpp:55-58
+        for (std::uint64_t i = 0; i < n; ++i) out[i] = dist(rng);
+    }
+}
+#define REF_KEYS(SUF, T)                                                                                    \
+    REF_API int ref_bench_keys_##SUF(std::uint64_t seed, std::uint64_t rank, std::uint64_t n, T* out) {     \
+        return guarded([&] { bench_keys_impl<T>(seed, rank, n, out); });                                   \
+    }
+REF_KEYS(i32, std::int32_t)
+REF_KEYS(u32, std::uint32_t)
+REF_KEYS(i64, std::int64_t)
+REF_KEYS(u64, std::uint64_t)
+REF_KEYS(f32, float)
+REF_KEYS(f64, double)
 
 REF_API std::uint64_t ref_sortperm_bytes(std::uint64_t n, int key_bytes, int index_bytes, int lowmem) {
     // sort.hpp:43-65 required_bytes formulas for equal-width instantiations

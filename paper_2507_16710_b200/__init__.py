@@ -581,6 +581,11 @@ class NcclComm:
     def handle(self):
         return self._h
 
+    def bytes_sent(self) -> int:
+        v = _U64()
+        _check(_fn("ak_comm_bytes_sent", [_P, C.POINTER(_U64)])(self._h, C.byref(v)))
+        return int(v.value)
+
     def allreduce_max(self, values: list[float], ex: ExecBackend) -> list[float]:
         arr = (C.c_double * len(values))(*values)
         _check(_fn("ak_comm_allreduce_max_f64", [_P, _P, _P, _U64])(self._h, ex.handle, arr, len(values)))
@@ -593,6 +598,81 @@ class NcclComm:
         if getattr(self, "_h", None):
             _fn("ak_comm_destroy", [_P])(self._h)
             self._h = None
+
+
+_AG_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+_AR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
+class IpcComm:
+    """rank_comm of one process per GPU whose bulk exchange is a peer-store kernel writing
+    straight into the peers' receive buffers (CUDA IPC mappings: P2P over NVLink/NVSwitch,
+    or the same GPU). Control messages (tiny allgather / allreduce) go over a torch.distributed
+    gloo group. Requires torch.distributed to be initialised (any backend)."""
+
+    def __init__(self, device: int, group=None):
+        import torch.distributed as dist
+        self._dist = dist
+        self.rank, self.size = dist.get_rank(), dist.get_world_size()
+        self._group = group if group is not None else dist.new_group(backend="gloo")
+        world = self.size
+
+        def ag(user, inp, nbytes, out):
+            try:
+                buf = torch.frombuffer(bytearray(C.string_at(inp, nbytes)), dtype=torch.uint8) if nbytes else \
+                    torch.empty(0, dtype=torch.uint8)
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, buf, group=self._group)
+                if nbytes:
+                    cat = torch.cat(outs).numpy()
+                    C.memmove(out, cat.ctypes.data, nbytes * world)
+                return 0
+            except Exception:  # pragma: no cover - surfaced as AK_ETRANSPORT
+                return 1
+
+        def ar(user, ptr, n):
+            try:
+                arr = np.frombuffer(C.string_at(ptr, 8 * n), dtype=np.int64).copy()
+                t = torch.from_numpy(arr)
+                dist.all_reduce(t, group=self._group)  # wrapping int64 sum == uint64 sum
+                C.memmove(ptr, t.numpy().ctypes.data, 8 * n)
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        self._cb = (_AG_FN(ag), _AR_FN(ar))
+        h = C.c_void_p()
+        _check(_fn("ak_comm_ipc_create", [C.c_int, C.c_int, C.c_int, _P, _AG_FN, _AR_FN, C.POINTER(C.c_void_p)])(
+            self.size, self.rank, device, None, self._cb[0], self._cb[1], C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def bytes_sent(self) -> int:
+        v = _U64()
+        _check(_fn("ak_comm_bytes_sent", [_P, C.POINTER(_U64)])(self._h, C.byref(v)))
+        return int(v.value)
+
+    def allreduce_max(self, values: list[float], ex: ExecBackend) -> list[float]:
+        arr = (C.c_double * len(values))(*values)
+        _check(_fn("ak_comm_allreduce_max_f64", [_P, _P, _P, _U64])(self._h, ex.handle, arr, len(values)))
+        return list(arr)
+
+    def barrier(self, ex: ExecBackend) -> None:
+        _check(_fn("ak_comm_barrier", [_P, _P])(self._h, ex.handle))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _fn("ak_comm_destroy", [_P])(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class LoopbackWorld:

@@ -2,6 +2,7 @@
 #include <climits>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <memory>
 #include <random>
 #include <string>
@@ -22,14 +23,14 @@
 
 struct ak_comm {
     std::unique_ptr<akb::comm_iface> impl;
-    akb::nccl_comm* nccl = nullptr;      // non-owning view when impl is NCCL
-    akb::loopback_comm* loop = nullptr;  // non-owning view when impl is a loopback rank
+    bool host_p2p = false;                      // loopback: messages never touch the device
+    std::map<int, std::vector<char>> pending;   // received message awaiting a larger buffer
 };
 
 // sim::world (sim_comm.hpp:41-80) on one device: P logical ranks, one host thread each.
 struct ak_world {
     akb::loopback_world w;
-    explicit ak_world(int ranks) : w(ranks) {}
+    ak_world(int ranks, std::size_t queue_capacity) : w(ranks, queue_capacity) {}
 };
 
 namespace {
@@ -254,8 +255,7 @@ void search_impl(ak_ctx* c, const T* hay, std::uint64_t n, const T* needles, std
 
 akb::comm_iface& comm_of(ak_comm* comm, self_comm& fallback, ak_ctx* c) {
     if (!comm) return fallback;
-    if (comm->nccl) comm->nccl->stream = c->stream;
-    if (comm->loop) comm->loop->stream = c->stream;
+    comm->impl->bind(c->stream, c->sm_count);
     return *comm->impl;
 }
 
@@ -305,6 +305,75 @@ void sihsort_host_impl(ak_ctx* c, ak_comm* comm, const T* h_in, std::uint64_t n,
     to_stats(st, stats);
 }
 
+// ---- sihsort stage functions (sihsort.hpp:264-501) ----
+template <typename T>
+void sample_local_impl(ak_ctx* c, const T* d, uint64_t n, uint64_t k, T* h, uint64_t* cnt) {
+    ctx_lock g(c);
+    need(cnt != nullptr, "sample_local: null count");
+    need(n == 0 || d, "sample_local: null input");
+    need(k == 0 || n == 0 || h, "sample_local: null output");
+    *cnt = akb::sample_local_device<T>(c, d, n, k, h);
+}
+
+template <typename T>
+void histogram_impl(const T* smp, uint64_t m, uint64_t bins, long double* e, uint64_t* cts, uint64_t cap,
+                    uint64_t* nb, uint64_t* tot) {
+    need(nb && tot && e && cts, "build_interpolated_histogram: null argument");
+    need(m == 0 || smp, "build_interpolated_histogram: null samples");
+    const akb::proto::histogram h = akb::proto::build_histogram(std::vector<T>(smp, smp + m), bins);
+    need(h.counts.size() <= cap, "build_interpolated_histogram: bin capacity too small");
+    std::copy(h.edges.begin(), h.edges.end(), e);
+    std::copy(h.counts.begin(), h.counts.end(), cts);
+    *nb = h.counts.size();
+    *tot = h.total;
+}
+
+template <typename T>
+void select_impl(const long double* e, const uint64_t* cts, uint64_t nb, uint64_t tot, uint64_t world, T* out) {
+    need(e && cts && nb >= 1, "select_splitters: empty histogram");
+    need(world <= 1 || out, "select_splitters: null output");
+    const auto v = akb::proto::select<T>(std::vector<long double>(e, e + nb + 1), std::vector<uint64_t>(cts, cts + nb),
+                                         tot, world);
+    std::copy(v.begin(), v.end(), out);
+}
+
+template <typename T>
+void refine_impl(ak_ctx* c, ak_comm* comm, const T* d, uint64_t n, T* spl, uint64_t m, const ak_sih_config* cfg,
+                 uint64_t* rounds, int* conv, double* dev) {
+    ctx_lock g(c);
+    need(n == 0 || d, "refine_splitters: null input");
+    need(m == 0 || spl, "refine_splitters: null splitters");
+    self_comm self;
+    akb::comm_iface& cm = comm_of(comm, self, c);
+    std::vector<T> v(spl, spl + m);
+    const akb::refine_out r = akb::refine_device<T>(c, cm, d, n, v, to_cfg(cfg));
+    std::copy(v.begin(), v.end(), spl);
+    if (rounds) *rounds = r.rounds_used;
+    if (conv) *conv = static_cast<int>(r.converged);
+    if (dev) *dev = r.max_deviation;
+}
+
+template <typename T>
+void redistribute_impl(ak_ctx* c, ak_comm* comm, const T* d, uint64_t n, const T* spl, uint64_t m, uint64_t nt,
+                       T* out, uint64_t cap, uint64_t* oc, uint64_t* sends, uint64_t* bytes) {
+    ctx_lock g(c);
+    need(oc != nullptr, "redistribute: null out_count");
+    need(n == 0 || d, "redistribute: null input");
+    need(m == 0 || spl, "redistribute: null splitters");
+    need(cap == 0 || out, "redistribute: null output");
+    self_comm self;
+    akb::comm_iface& cm = comm_of(comm, self, c);
+    uint64_t s0 = 0, b0 = 0;
+    try {
+        *oc = akb::redistribute_device<T>(c, cm, d, n, std::vector<T>(spl, spl + m), out, cap, &s0, &b0, nt);
+    } catch (const akb::proto_capacity_error& e) {
+        *oc = e.required;
+        throw;
+    }
+    if (sends) *sends = s0;
+    if (bytes) *bytes = b0;
+}
+
 template <typename T>
 void sihsort_loopback_impl(int device, std::uint64_t P, const T* const* in, const std::uint64_t* n,
                            T* const* out, const std::uint64_t* cap, std::uint64_t* out_count,
@@ -322,6 +391,7 @@ void sihsort_loopback_impl(int device, std::uint64_t P, const T* const* in, cons
             try {
                 if (ak_ctx_create(device, nullptr, &ctx) != AK_OK) throw akb::cuda_error(g_err);
                 akb::loopback_comm cm(&world, static_cast<int>(r), ctx->stream);
+                cm.bind(ctx->stream, ctx->sm_count);
                 akb::sih_stats_c st{};
                 {
                     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -677,6 +747,26 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int kb) {
                                 T* const* out, const uint64_t* cap, uint64_t* oc,                       \
                                 const ak_sih_config* cfg, ak_sih_stats* st) {                           \
         return guard([&] { sihsort_loopback_impl<T>(dev, P, in, n, out, cap, oc, cfg, st); });           \
+    }                                                                                                    \
+    int ak_sample_local_##S(ak_ctx* c, const T* d, uint64_t n, uint64_t k, T* h, uint64_t* cnt) {        \
+        return guard([&] { sample_local_impl<T>(c, d, n, k, h, cnt); });                                \
+    }                                                                                                    \
+    int ak_build_interpolated_histogram_##S(const T* smp, uint64_t m, uint64_t bins, long double* e,     \
+                                            uint64_t* cts, uint64_t cap, uint64_t* nb, uint64_t* tot) {  \
+        return guard([&] { histogram_impl<T>(smp, m, bins, e, cts, cap, nb, tot); });                   \
+    }                                                                                                    \
+    int ak_select_splitters_##S(const long double* e, const uint64_t* cts, uint64_t nb, uint64_t tot,    \
+                                uint64_t world, T* out) {                                                \
+        return guard([&] { select_impl<T>(e, cts, nb, tot, world, out); });                              \
+    }                                                                                                    \
+    int ak_refine_splitters_##S(ak_ctx* c, ak_comm* cm, const T* d, uint64_t n, T* spl, uint64_t m,      \
+                                const ak_sih_config* cfg, uint64_t* rounds, int* conv, double* dev) {    \
+        return guard([&] { refine_impl<T>(c, cm, d, n, spl, m, cfg, rounds, conv, dev); });              \
+    }                                                                                                    \
+    int ak_redistribute_##S(ak_ctx* c, ak_comm* cm, const T* d, uint64_t n, const T* spl, uint64_t m,    \
+                            uint64_t nt, T* out, uint64_t cap, uint64_t* oc, uint64_t* sends,            \
+                            uint64_t* bytes) {                                                           \
+        return guard([&] { redistribute_impl<T>(c, cm, d, n, spl, m, nt, out, cap, oc, sends, bytes); }); \
     }
 
 AK_DEFINE(i32, int32_t)
@@ -777,7 +867,6 @@ int ak_comm_nccl_create(const void* uid, int nranks, int rank, int device, ak_co
         impl->p = nranks;
         impl->device = device;
         auto c = std::make_unique<ak_comm>();
-        c->nccl = impl.get();
         c->impl = std::move(impl);
         *out = c.release();
     });
@@ -794,11 +883,99 @@ int ak_comm_callbacks_create(int nranks, int rank, void* user, ak_allgather_fn a
     });
 }
 
-int ak_world_create(int ranks, ak_world** out) {
+int ak_comm_ipc_create(int nranks, int rank, int device, void* user, ak_allgather_fn ag, ak_allreduce_u64_fn ar,
+                       ak_comm** out) {
+    return guard([&] {
+        need(out && ag && ar, "ak_comm_ipc_create: null argument");
+        need(nranks >= 1 && rank >= 0 && rank < nranks, "ak_comm_ipc_create: bad rank");
+        int ndev = 0;
+        AKB_CUDA(cudaGetDeviceCount(&ndev));
+        need(device >= 0 && device < ndev, "ak_comm_ipc_create: bad device");
+        auto c = std::make_unique<ak_comm>();
+        c->impl = std::make_unique<akb::ipc_comm>(rank, nranks, device, user, ag, ar);
+        *out = c.release();
+    });
+}
+
+int ak_comm_bytes_sent(const ak_comm* comm, uint64_t* out) {
+    return guard([&] {
+        need(comm && out, "ak_comm_bytes_sent: null argument");
+        *out = comm->impl->payload_bytes_sent();
+    });
+}
+
+int ak_world_create(int ranks, ak_world** out) { return ak_world_create_ex(ranks, 64, out); }
+
+int ak_world_create_ex(int ranks, uint64_t queue_capacity, ak_world** out) {
     return guard([&] {
         need(out != nullptr, "ak_world_create: null output");
-        need(ranks >= 1, "world: rank count must be >= 1");  // sim_comm.cpp:7-9
-        *out = new ak_world(ranks);
+        need(ranks >= 1, "world: rank count must be >= 1");              // sim_comm.cpp:7-9
+        need(queue_capacity >= 1, "world: queue capacity must be >= 1");  // sim_comm.cpp:10-12
+        *out = new ak_world(ranks, queue_capacity);
+    });
+}
+
+int ak_comm_send(ak_comm* comm, ak_ctx* c, int dest, const void* bytes, uint64_t n, int control) {
+    return guard([&] {
+        need(comm != nullptr, "send: null communicator");
+        need(n == 0 || bytes, "send: null message");
+        if (comm->host_p2p) {
+            comm->impl->send_bytes(dest, bytes, n, control != 0);
+            return;
+        }
+        ctx_lock g(c);
+        self_comm self;
+        comm_of(comm, self, c).send_bytes(dest, bytes, n, control != 0);
+    });
+}
+
+int ak_comm_recv(ak_comm* comm, ak_ctx* c, int src, void* buf, uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        need(comm && n, "recv: null argument");
+        auto it = comm->pending.find(src);
+        if (it == comm->pending.end()) {
+            std::vector<char> m;
+            if (comm->host_p2p) {
+                m = comm->impl->recv_bytes(src);
+            } else {
+                ctx_lock g(c);
+                self_comm self;
+                m = comm_of(comm, self, c).recv_bytes(src);
+            }
+            it = comm->pending.emplace(src, std::move(m)).first;
+        }
+        *n = it->second.size();
+        if (it->second.size() > cap) throw akb::capacity_error("recv: message larger than the buffer", *n);
+        if (*n) std::memcpy(buf, it->second.data(), *n);
+        comm->pending.erase(it);
+    });
+}
+
+int ak_comm_allgather(ak_comm* comm, ak_ctx* c, const void* in, uint64_t bytes, void* out) {
+    return guard([&] {
+        need(bytes == 0 || (in && out), "allgather: null argument");
+        if (comm && comm->host_p2p) {  // host-level collective: no ctx lock (ranks share no device state)
+            comm->impl->allgather(in, bytes, out);
+            comm->impl->count_collective();
+            return;
+        }
+        ctx_lock g(c);
+        self_comm self;
+        akb::comm_iface& cm = comm_of(comm, self, c);
+        cm.allgather(in, bytes, out);
+        cm.count_collective();
+    });
+}
+
+int ak_comm_counters(const ak_comm* comm, ak_rank_counters* out) {
+    return guard([&] {
+        need(comm && out, "counters: null argument");
+        const auto k = comm->impl->counters();
+        out->p2p_sends = k.p2p_sends;
+        out->p2p_bytes = k.p2p_bytes;
+        out->collective_ops = k.collective_ops;
+        out->collective_sends = k.collective_sends;
+        out->control_bytes_peak = k.control_bytes_peak;
     });
 }
 
@@ -821,7 +998,7 @@ int ak_comm_loopback_create(ak_world* w, int rank, ak_comm** out) {
         need(rank >= 0 && rank < w->w.P, "rank_comm: rank out of range");  // sim_comm.cpp:11-13
         auto impl = std::make_unique<akb::loopback_comm>(&w->w, rank, nullptr);
         auto c = std::make_unique<ak_comm>();
-        c->loop = impl.get();
+        c->host_p2p = true;
         c->impl = std::move(impl);
         *out = c.release();
     });

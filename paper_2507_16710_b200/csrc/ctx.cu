@@ -1,6 +1,10 @@
 // ctx.cu -- handle lifetime and scratch management.
 #include "ctx.cuh"
 
+#include <mutex>
+#include <set>
+#include <tuple>
+
 namespace akb {
 
 void ctx_reserve_aux(ak_ctx* c, std::size_t bytes) {
@@ -119,6 +123,19 @@ void ctx_prof_resolve(ak_ctx* c) {
         c->event_pool.push_back({t.a, t.b});
     }
     c->pending.clear();
+}
+
+void func_attr_once(const ak_ctx* c, const void* func, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int, int>> done;  // (func, device, attr, value)
+    const auto key = std::make_tuple(func, c->device, static_cast<int>(attr), value);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(key)) return;
+    int cur = -1;
+    AKB_CUDA(cudaGetDevice(&cur));
+    if (cur != c->device) AKB_CUDA(cudaSetDevice(c->device));
+    AKB_CUDA(cudaFuncSetAttribute(func, attr, value));
+    done.insert(key);
 }
 
 void* ctx_stage(ak_ctx* c, std::size_t bytes) {

@@ -114,6 +114,14 @@ std::uint64_t* ctx_cuts(ak_ctx* c, std::size_t count);
 std::uint64_t* ctx_msd(ak_ctx* c);
 std::uint64_t* ctx_msd3(ak_ctx* c);
 void* ctx_stage(ak_ctx* c, std::size_t bytes);
+// Kernel attributes live in each device's context: set `func`'s attribute once per device
+// (a process may drive several GPUs, one ctx each, from several threads).
+void func_attr_once(const ak_ctx* c, const void* func, cudaFuncAttribute attr, int value);
+template <typename F>
+inline void smem_attr(const ak_ctx* c, F* func, std::size_t bytes) {
+    func_attr_once(c, reinterpret_cast<const void*>(func), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                   static_cast<int>(bytes));
+}
 // ctx-owned work arena (grown on demand, reused); nullptr when the allocation fails
 void* ctx_work(ak_ctx* c, std::size_t bytes);
 

@@ -457,15 +457,9 @@ __global__ void __launch_bounds__(1024) scan24_chunk_kernel(const std::uint32_t*
 template <typename T>
 void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint,
               bool digit5) {
-    static bool configured = false;
     constexpr std::size_t smem = JOINT_BINS * 2 + 256 * JH_PARTS * 4;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(hist_joint_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        AKB_CUDA(cudaFuncSetAttribute(hist_joint_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        configured = true;
-    }
+    smem_attr(c, hist_joint_kernel<T, true>, smem);
+    smem_attr(c, hist_joint_kernel<T, false>, smem);
     AKB_CUDA(cudaMemsetAsync(g_joint, 0, JOINT_BINS * sizeof(std::uint64_t), c->stream));
     const int tok = ctx_prof_begin(c, KF_HIST);
     if (digit5)
@@ -486,14 +480,8 @@ void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t
 template <typename T>
 void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool desc, const std::uint64_t* g_joint,
                std::uint64_t* cur16, std::uint64_t* cur8) {
-    static bool configured = false;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(msd_pass_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(mp_smem::total)));
-        AKB_CUDA(cudaFuncSetAttribute(msd_pass_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(mp_smem::total)));
-        configured = true;
-    }
+    smem_attr(c, msd_pass_kernel<T, 1>, mp_smem::total);
+    smem_attr(c, msd_pass_kernel<T, 2>, mp_smem::total);
     const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
     int tok = ctx_prof_begin(c, KF_MSD);
     msd_pass_kernel<T, 1><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kmid, n, desc ? 1 : 0, cur8);
@@ -508,12 +496,7 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
 
 template <typename T>
 void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc) {
-    static bool configured = false;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(msd_pass_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(mp_smem::total)));
-        configured = true;
-    }
+    smem_attr(c, msd_pass_kernel<T, 3>, mp_smem::total);
     std::uint64_t* cur24 = ctx_msd3(c);                                   // 2^24 u64 cursors
     std::uint32_t* hist24 = reinterpret_cast<std::uint32_t*>(cur24 + (1u << 24));  // 2^24 u32 counts
     std::uint64_t* sums = cur24 + (1u << 24) + (1u << 23);               // 4096 chunk sums

@@ -639,30 +639,19 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     AKB_PHASE(5);
 }
 
-int match_kind_env() {
-    static const int k = [] {
-        const char* e = std::getenv("AKB_MATCH");
-        if (e && std::strcmp(e, "hw") == 0) return static_cast<int>(MATCH_HW);
-        if (e && std::strcmp(e, "ballot") == 0) return static_cast<int>(MATCH_BALLOT);
-        if (e && std::strcmp(e, "smem") == 0) return static_cast<int>(MATCH_SMEM);
-        if (e && std::strcmp(e, "hybrid") == 0) return static_cast<int>(MATCH_HYBRID);
-        if (e && std::strcmp(e, "half") == 0) return static_cast<int>(MATCH_HALF);
-        return static_cast<int>(MATCH_HALF);  // r01 sweep: half 12.97 / hybrid 13.12 / smem 13.35 / ballot 14.5 / hw 18.6 ms
-    }();
-    return k;
-}
+// Ranking variant of the onesweep pass (experiment builds: -DAKB_CFG_MATCH=...). r01 sweep,
+// 2^28 int64 full sort: half 12.97 / hybrid 13.12 / smem 13.35 / ballot 14.5 / hw 18.6 ms.
+#ifndef AKB_CFG_MATCH
+#define AKB_CFG_MATCH MATCH_HALF
+#endif
 
 template <typename T, typename V, int MODE, int HW>
 void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift,
                       bool desc, int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter,
                       bool write_keys) {
     using L = pass_smem<T, V, MODE>;
-    static bool configured = false;
     auto kern = onesweep_kernel<T, V, MODE, HW>;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L::total)));
-        configured = true;
-    }
+    smem_attr(c, kern, L::total);
     const std::uint64_t tiles = ceil_div(n, L::TILE);
     const std::uint32_t tag = ctx_lookback_pass(c, tiles);
     const int tok = ctx_prof_begin(c, KF_ONESWEEP);
@@ -677,27 +666,8 @@ void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, s
 template <typename T, typename V, int MODE>
 void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift, bool desc,
                  int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter, bool write_keys) {
-    switch (match_kind_env()) {
-        case MATCH_HW:
-            launch_pass_impl<T, V, MODE, MATCH_HW>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                                   tile_counter, write_keys);
-            break;
-        case MATCH_BALLOT:
-            launch_pass_impl<T, V, MODE, MATCH_BALLOT>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                                       tile_counter, write_keys);
-            break;
-        case MATCH_HALF:
-            launch_pass_impl<T, V, MODE, MATCH_HALF>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                                     tile_counter, write_keys);
-            break;
-        case MATCH_HYBRID:
-            launch_pass_impl<T, V, MODE, MATCH_HYBRID>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                                      tile_counter, write_keys);
-            break;
-        default:
-            launch_pass_impl<T, V, MODE, MATCH_SMEM>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                                     tile_counter, write_keys);
-    }
+    launch_pass_impl<T, V, MODE, AKB_CFG_MATCH>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
+                                                tile_counter, write_keys);
 }
 
 template <typename T, typename V, int MODE>
@@ -1436,32 +1406,23 @@ __global__ void bucket_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, 
     cuts[j] = lo;
 }
 
-int msd_env() {
-    static const int v = [] {
-        const char* e = std::getenv("AKB_MSD");  // "0": stable onesweep top-digit passes
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
+// 0: stable onesweep top-digit passes instead of the MSD partition (experiment builds: make variant DEFS=-DAKB_CFG_MSD=...)
+#ifndef AKB_CFG_MSD
+#define AKB_CFG_MSD 1
+#endif
+constexpr int msd_env() { return AKB_CFG_MSD; }
 
-int hybrid_env() {
-    static const int v = [] {
-        const char* e = std::getenv("AKB_HYBRID");  // "0" disables (plain LSD), "m" forces m top passes
-        return e ? std::atoi(e) : -1;
-    }();
-    return v;
-}
+// 0: plain LSD; m > 0: force m top passes; -1: planned from the data (experiment builds: make variant DEFS=-DAKB_CFG_HYBRID=...)
+#ifndef AKB_CFG_HYBRID
+#define AKB_CFG_HYBRID -1
+#endif
+constexpr int hybrid_env() { return AKB_CFG_HYBRID; }
 
 template <typename T, int ITEMS>
 void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc, int low,
                   std::uint64_t* big) {
     using LS = local_smem<T, ITEMS>;
-    static bool configured = false;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(local_sort_kernel<T, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(LS::total)));
-        configured = true;
-    }
+    smem_attr(c, local_sort_kernel<T, ITEMS>, LS::total);
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     local_sort_kernel<T, ITEMS><<<static_cast<unsigned>(J), LOCAL_BLOCK, LS::total, c->stream>>>(
         G, kout, cuts, desc ? 1 : 0, low, big);
@@ -1620,13 +1581,11 @@ __global__ void mc_maxtile_kernel(const std::uint64_t* __restrict__ pos, int P, 
     if ((threadIdx.x & 31) == 0 && t) atomicMax(mx, static_cast<unsigned long long>(t));
 }
 
-int local_count_env() {
-    static const int v = [] {
-        const char* e = std::getenv("AKB_LOCAL_COUNT");  // "0": stable radix local stage for every range
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
+// 0: stable radix local stage for every range (experiment builds: make variant DEFS=-DAKB_CFG_LOCAL_COUNT=...)
+#ifndef AKB_CFG_LOCAL_COUNT
+#define AKB_CFG_LOCAL_COUNT 1
+#endif
+constexpr int local_count_env() { return AKB_CFG_LOCAL_COUNT; }
 
 // Counting local stage (integer keys only), then the stable radix kernel over the ranges
 // it handed back (persistent loop over redo[1 .. redo[0]]; no host round trip).
@@ -1637,16 +1596,9 @@ void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cut
     static_assert(CITEMS * LC_BLOCK == ITEMS * LOCAL_BLOCK, "same range capacity");
     using CS = lc_smem<T, CITEMS>;
     using LS = local_smem<T, ITEMS>;
-    static bool configured = false;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(local_count_kernel<T, CITEMS, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CS::total)));
-        AKB_CUDA(cudaFuncSetAttribute(local_count_kernel<T, CITEMS, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CS::total)));
-        AKB_CUDA(cudaFuncSetAttribute(local_redo_kernel<T, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(LS::total)));
-        configured = true;
-    }
+    smem_attr(c, local_count_kernel<T, CITEMS, false>, CS::total);
+    smem_attr(c, local_count_kernel<T, CITEMS, true>, CS::total);
+    smem_attr(c, local_redo_kernel<T, ITEMS>, LS::total);
     AKB_CUDA(cudaMemsetAsync(redo, 0, sizeof(std::uint64_t), c->stream));
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * CS::MINB));
@@ -1845,10 +1797,12 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     AKB_CUDA(cudaGetLastError());
     c->kernel_launches += 1;
     // local radix passes cover the two digits under the bucket digits; the rest is the
-    // run fix-up (AKB_LOCAL_LOW overrides: 0 = radix-pass every varying digit)
+    // run fix-up (experiment builds: -DAKB_CFG_LOCAL_LOW=0 radix-passes every varying digit)
     int low = top - m - 2;
     if (low < 0) low = 0;
-    if (const char* e = std::getenv("AKB_LOCAL_LOW")) low = std::atoi(e);
+#ifdef AKB_CFG_LOCAL_LOW
+    low = AKB_CFG_LOCAL_LOW;
+#endif
     bool counted = false;
     if constexpr (std::is_integral_v<T> && sizeof(T) == 8) {  // the only keys that reach here (see above)
         if (local_count_env() != 0) {
@@ -1899,13 +1853,11 @@ bool hybrid_sort_keys(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n
     else return false;
 }
 
-int merge_count_env() {
-    static const int v = [] {
-        const char* e = std::getenv("AKB_MERGE_COUNT");  // "0": always the merge-path tree
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
+// 0: always the merge-path tree (experiment builds: make variant DEFS=-DAKB_CFG_MERGE_COUNT=...)
+#ifndef AKB_CFG_MERGE_COUNT
+#define AKB_CFG_MERGE_COUNT 1
+#endif
+constexpr int merge_count_env() { return AKB_CFG_MERGE_COUNT; }
 
 template <typename T>
 bool merge_runs_counting_impl(ak_ctx* c, int P, const T* const* runs, const std::uint64_t* lens, T* dst, bool desc) {
@@ -1958,14 +1910,8 @@ bool merge_runs_counting_impl(ak_ctx* c, int P, const T* const* runs, const std:
     if (h[0] > CAPK) return false;  // heavy ties: the merge-path tree
     std::uint64_t* big = ctx_cuts(c, J + 2);
     AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
-    static bool configured = false;
-    if (!configured) {
-        AKB_CUDA(cudaFuncSetAttribute(merge_count_kernel<T, ITEMS, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(MS::total)));
-        AKB_CUDA(cudaFuncSetAttribute(merge_count_kernel<T, ITEMS, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(MS::total)));
-        configured = true;
-    }
+    smem_attr(c, merge_count_kernel<T, ITEMS, false>, MS::total);
+    smem_attr(c, merge_count_kernel<T, ITEMS, true>, MS::total);
     const int tok = ctx_prof_begin(c, KF_MERGE);
     if (desc)
         merge_count_kernel<T, ITEMS, true><<<static_cast<unsigned>(J), LC_BLOCK, MS::total, c->stream>>>(d_runs, P, pos,

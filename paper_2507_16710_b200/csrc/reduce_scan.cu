@@ -439,16 +439,11 @@ void scan(ak_ctx* c, const T* x, T* out, std::uint64_t n, int op, int inclusive,
     AKB_CUDA(cudaMemsetAsync(counter, 0, 4, c->stream));
     const int tok = ctx_prof_begin(c, KF_SCAN);
     const bool vecio = ((reinterpret_cast<std::uintptr_t>(x) | reinterpret_cast<std::uintptr_t>(out)) & 15) == 0;
-    // 6 x 32 KB tiles per SM: ask for the full shared-memory carveout once per instantiation
+    // 6 x 32 KB tiles per SM: ask for the full shared-memory carveout (once per device)
 #define AKB_SCAN(OPV, V)                                                                       \
     do {                                                                                       \
-        static bool carve = false;                                                             \
-        if (!carve) {                                                                          \
-            AKB_CUDA(cudaFuncSetAttribute(scan_kernel<T, OPV, V>,                              \
-                                          cudaFuncAttributePreferredSharedMemoryCarveout,      \
-                                          cudaSharedmemCarveoutMaxShared));                    \
-            carve = true;                                                                      \
-        }                                                                                      \
+        func_attr_once(c, reinterpret_cast<const void*>(scan_kernel<T, OPV, V>),              \
+                       cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared); \
         scan_kernel<T, OPV, V><<<static_cast<unsigned>(tiles), scan_cfg<T>::BLOCK, 0, c->stream>>>(     \
             x, out, n, init, inclusive, c->scan_flags, c->scan_vals, tag, counter);            \
     } while (0)

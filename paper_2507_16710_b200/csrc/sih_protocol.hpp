@@ -76,6 +76,45 @@ struct comm_iface {
                           const std::uint64_t* recv_off, const std::uint64_t* recv_cnt,
                           std::size_t elem_bytes) = 0;
     virtual void abort() noexcept {}
+    // the caller's ctx stream (cudaStream_t) and SM count, set before every call that
+    // may use the transport (device transports enqueue their copies there)
+    virtual void bind(void* /*stream*/, int /*sm_count*/) {}
+    // bulk payload bytes this rank has pushed to peers through exchange() (counters)
+    virtual std::uint64_t payload_bytes_sent() const { return 0; }
+    // user point-to-point messages of rank_comm::send / recv (sim_comm.hpp:92-121): host
+    // bytes, FIFO per ordered pair; control = traffic_class::control
+    virtual void send_bytes(int /*dest*/, const void* /*p*/, std::size_t /*n*/, bool /*control*/) {
+        throw std::runtime_error("transport: point-to-point messages are not supported by this communicator");
+    }
+    virtual std::vector<char> recv_bytes(int /*src*/) {
+        throw std::runtime_error("transport: point-to-point messages are not supported by this communicator");
+    }
+    // rank_counters (sim_comm.hpp:33-39)
+    struct counters_c {
+        std::uint64_t p2p_sends = 0, p2p_bytes = 0, collective_ops = 0, collective_sends = 0,
+                      control_bytes_peak = 0;
+    };
+    virtual counters_c counters() const { return ctr; }
+    // one collective of the reference's accounting: 1 op, and the messages this rank would
+    // send in its binomial reduce-to-0 + broadcast tree (sim_comm.hpp:124-149)
+    void count_collective() {
+        ctr.collective_ops += 1;
+        ctr.collective_sends += tree_sends(rank(), size());
+    }
+    static std::uint64_t tree_sends(int r, int p) {
+        std::uint64_t s = 0;
+        int m = 1;
+        while (m * 2 < p) m *= 2;
+        for (; m >= 1; m >>= 1)
+            if (r >= m && r < 2 * m) {
+                ++s;
+                break;
+            }
+        for (m = 1; m < p; m <<= 1)
+            if (r < m && r + m < p) ++s;
+        return s;
+    }
+    counters_c ctr;
 };
 
 // Callback-backed transport: lets any runtime (torch.distributed, MPI, ...)
@@ -158,6 +197,32 @@ void count_bins(const std::vector<T>& samples, const std::vector<long double>& e
         }
         ++counts[bin];
     }
+}
+
+// build_interpolated_histogram (sihsort.hpp:286-305) over a rank's gathered samples
+struct histogram {
+    std::vector<long double> edges;
+    std::vector<std::uint64_t> counts;
+    std::uint64_t total = 0;
+};
+template <typename T>
+histogram build_histogram(const std::vector<T>& samples, std::size_t bins) {
+    histogram h;
+    if (samples.empty() || bins == 0) {
+        h.edges = {0.0L, 0.0L};
+        h.counts = {0};
+        return h;
+    }
+    T lo = samples[0], hi = samples[0];
+    for (const T& v : samples) {
+        if (v < lo) lo = v;
+        if (hi < v) hi = v;
+    }
+    h.edges = edges(to_ld(lo), to_ld(hi), bins);
+    h.counts.assign(h.edges.size() - 1, 0);
+    count_bins(samples, h.edges, h.counts);
+    h.total = samples.size();
+    return h;
 }
 
 // select_splitters (sihsort.hpp:310-349)
@@ -245,6 +310,133 @@ bool tail_mode(std::uint64_t n_total) {
 
 }  // namespace proto
 
+struct refine_out {
+    std::uint64_t rounds_used = 0;
+    std::uint64_t converged = 0;
+    double max_deviation = 0.0;
+    std::uint64_t collectives = 0;
+};
+
+// refine_splitters (sihsort.hpp:364-464) on a rank whose sorted keys the policy holds (n keys,
+// local min / max data_min / data_max when n > 0); spl is refined in place. Collective.
+template <typename T, typename Local>
+refine_out refine_run(comm_iface& comm, Local& L, std::vector<T>& spl, std::uint64_t n, T data_min, T data_max,
+                      const sih_config_c& cfg) {
+    refine_out st;
+    const std::size_t P = static_cast<std::size_t>(comm.size());
+    if (cfg.max_refine_rounds == 0) return st;
+    proto::summary<T> rs;
+    rs.n = n;
+    if (n > 0) {
+        rs.data_min = data_min;
+        rs.data_max = data_max;
+    }
+    const proto::summary<T> s2 = proto::global_summary(comm, rs);
+    ++st.collectives;
+    const std::uint64_t n_total = s2.n;
+    if (P <= 1 || spl.empty() || n_total == 0) {
+        st.converged = 1;
+        return st;
+    }
+    const long double ideal = static_cast<long double>(n_total) / static_cast<long double>(P);
+    std::vector<T> lo(P - 1, s2.data_min), hi(P - 1, s2.data_max);
+    std::vector<std::uint64_t> flo(P - 1, 0), fhi(P - 1, n_total);
+    std::vector<bool> frozen(P - 1, false);
+    std::vector<std::uint64_t> le;
+    for (std::size_t round = 1; round <= cfg.max_refine_rounds; ++round) {
+        L.upper_bounds(spl, le);
+        comm.allreduce_sum_u64(le.data(), le.size());
+        ++st.collectives;
+        long double max_dev = 0.0L;
+        for (std::size_t r = 0; r < P; ++r) {
+            const std::uint64_t upper = r + 1 < P ? le[r] : n_total;
+            const std::uint64_t lower = r > 0 ? le[r - 1] : 0;
+            const long double bucket = static_cast<long double>(upper - lower);
+            max_dev = std::max(max_dev, std::abs(bucket - ideal) / ideal);
+        }
+        st.rounds_used = round;
+        st.max_deviation = static_cast<double>(max_dev);
+        if (max_dev <= static_cast<long double>(cfg.imbalance_tol)) {
+            st.converged = 1;
+            break;
+        }
+        if (round == cfg.max_refine_rounds) break;
+        for (std::size_t j = 0; j + 1 < P; ++j) {
+            if (frozen[j]) continue;
+            const long double target = ideal * static_cast<long double>(j + 1);
+            const std::uint64_t measured = le[j];
+            if (static_cast<long double>(measured) < target) {
+                lo[j] = spl[j];
+                flo[j] = measured;
+            } else if (static_cast<long double>(measured) > target) {
+                hi[j] = spl[j];
+                fhi[j] = measured;
+            } else {
+                frozen[j] = true;
+                continue;
+            }
+            if (!(lo[j] < hi[j]) || fhi[j] <= flo[j]) {
+                frozen[j] = true;
+                continue;
+            }
+            const long double frac = (target - static_cast<long double>(flo[j])) /
+                                     static_cast<long double>(fhi[j] - flo[j]);
+            const long double cand = proto::to_ld(lo[j]) + (proto::to_ld(hi[j]) - proto::to_ld(lo[j])) * frac;
+            T key = proto::ld_to_key<T>(cand);
+            if constexpr (std::is_integral_v<T>) {
+                if (key <= lo[j]) key = static_cast<T>(lo[j] + 1);
+                if (hi[j] < key) key = hi[j];
+            } else {
+                if (!(key > lo[j]) || !(key < hi[j]))
+                    key = proto::ld_to_key<T>((proto::to_ld(lo[j]) + proto::to_ld(hi[j])) / 2);
+                if (!(key > lo[j]) || !(key < hi[j])) {
+                    frozen[j] = true;
+                    continue;
+                }
+            }
+            spl[j] = key;
+        }
+        for (std::size_t j = 1; j + 1 < P; ++j)
+            if (spl[j] < spl[j - 1]) spl[j] = spl[j - 1];
+    }
+    return st;
+}
+
+// slice_bounds + P x P count exchange (with every rank's capacity) of redistribute
+// (sihsort.hpp:110-123, :472-501): bounds (P+1) of this rank's slices, recv_counts (P) it
+// receives from each source. Throws proto_capacity_error (on every rank alike) when some rank's
+// capacity is short. Collective.
+template <typename T, typename Local>
+void count_exchange(comm_iface& comm, Local& L, const std::vector<T>& spl, std::uint64_t n, std::uint64_t capacity,
+                    std::vector<std::uint64_t>& bounds, std::vector<std::uint64_t>& recv_counts) {
+    const std::size_t P = static_cast<std::size_t>(comm.size());
+    const std::size_t me = static_cast<std::size_t>(comm.rank());
+    bounds.assign(P + 1, 0);
+    {
+        std::vector<std::uint64_t> cuts;
+        L.upper_bounds(spl, cuts);
+        for (std::size_t j = 0; j + 1 < P; ++j) bounds[j + 1] = cuts[j];
+        bounds[P] = n;
+    }
+    // P x (P+1) matrix: row r = send counts of rank r to each dest, then its capacity
+    std::vector<std::uint64_t> row(P + 1), mat((P + 1) * P);
+    for (std::size_t d = 0; d < P; ++d) row[d] = bounds[d + 1] - bounds[d];
+    row[P] = capacity;
+    comm.allgather(row.data(), row.size() * sizeof(std::uint64_t), mat.data());
+    recv_counts.assign(P, 0);
+    for (std::size_t s = 0; s < P; ++s) recv_counts[s] = mat[s * (P + 1) + me];
+    for (std::size_t r = 0; r < P; ++r) {
+        std::uint64_t need = 0;
+        for (std::size_t s = 0; s < P; ++s) need += mat[s * (P + 1) + r];
+        if (need > mat[r * (P + 1) + P]) {
+            std::uint64_t mine_need = 0;
+            for (std::size_t s = 0; s < P; ++s) mine_need += recv_counts[s];
+            throw proto_capacity_error("sihsort: output capacity too small on rank " + std::to_string(r),
+                                       mine_need);
+        }
+    }
+}
+
 // The whole per-rank protocol (sihsort.hpp:508-559).
 template <typename T, typename Local>
 void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_c& st,
@@ -302,109 +494,21 @@ void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_
     }
 
     // refine_splitters (sihsort.hpp:364-464)
-    if (cfg.max_refine_rounds > 0) {
-        proto::summary<T> rs;
-        rs.n = n;
-        if (n > 0) {
-            rs.data_min = mine.data_min;
-            rs.data_max = mine.data_max;
-        }
-        const proto::summary<T> s2 = proto::global_summary(comm, rs);
-        ++collectives;
-        const std::uint64_t n_total = s2.n;
-        if (P <= 1 || spl.empty() || n_total == 0) {
-            st.converged = 1;
-        } else {
-            const long double ideal = static_cast<long double>(n_total) / static_cast<long double>(P);
-            std::vector<T> lo(P - 1, s2.data_min), hi(P - 1, s2.data_max);
-            std::vector<std::uint64_t> flo(P - 1, 0), fhi(P - 1, n_total);
-            std::vector<bool> frozen(P - 1, false);
-            std::vector<std::uint64_t> le;
-            for (std::size_t round = 1; round <= cfg.max_refine_rounds; ++round) {
-                L.upper_bounds(spl, le);
-                comm.allreduce_sum_u64(le.data(), le.size());
-                ++collectives;
-                long double max_dev = 0.0L;
-                for (std::size_t r = 0; r < P; ++r) {
-                    const std::uint64_t upper = r + 1 < P ? le[r] : n_total;
-                    const std::uint64_t lower = r > 0 ? le[r - 1] : 0;
-                    const long double bucket = static_cast<long double>(upper - lower);
-                    max_dev = std::max(max_dev, std::abs(bucket - ideal) / ideal);
-                }
-                st.rounds_used = round;
-                st.max_deviation = static_cast<double>(max_dev);
-                if (max_dev <= static_cast<long double>(cfg.imbalance_tol)) {
-                    st.converged = 1;
-                    break;
-                }
-                if (round == cfg.max_refine_rounds) break;
-                for (std::size_t j = 0; j + 1 < P; ++j) {
-                    if (frozen[j]) continue;
-                    const long double target = ideal * static_cast<long double>(j + 1);
-                    const std::uint64_t measured = le[j];
-                    if (static_cast<long double>(measured) < target) {
-                        lo[j] = spl[j];
-                        flo[j] = measured;
-                    } else if (static_cast<long double>(measured) > target) {
-                        hi[j] = spl[j];
-                        fhi[j] = measured;
-                    } else {
-                        frozen[j] = true;
-                        continue;
-                    }
-                    if (!(lo[j] < hi[j]) || fhi[j] <= flo[j]) {
-                        frozen[j] = true;
-                        continue;
-                    }
-                    const long double frac = (target - static_cast<long double>(flo[j])) /
-                                             static_cast<long double>(fhi[j] - flo[j]);
-                    const long double cand =
-                        proto::to_ld(lo[j]) + (proto::to_ld(hi[j]) - proto::to_ld(lo[j])) * frac;
-                    T key = proto::ld_to_key<T>(cand);
-                    if constexpr (std::is_integral_v<T>) {
-                        if (key <= lo[j]) key = static_cast<T>(lo[j] + 1);
-                        if (hi[j] < key) key = hi[j];
-                    } else {
-                        if (!(key > lo[j]) || !(key < hi[j]))
-                            key = proto::ld_to_key<T>((proto::to_ld(lo[j]) + proto::to_ld(hi[j])) / 2);
-                        if (!(key > lo[j]) || !(key < hi[j])) {
-                            frozen[j] = true;
-                            continue;
-                        }
-                    }
-                    spl[j] = key;
-                }
-                for (std::size_t j = 1; j + 1 < P; ++j)
-                    if (spl[j] < spl[j - 1]) spl[j] = spl[j - 1];
-            }
-        }
+    {
+        refine_out r = refine_run<T>(comm, L, spl, n, mine.data_min, mine.data_max, cfg);
+        collectives += r.collectives;
+        st.rounds_used = r.rounds_used;
+        st.converged = r.converged;
+        st.max_deviation = r.max_deviation;
     }
 
     // redistribute (sihsort.hpp:472-501): slice_bounds + count exchange + payload
-    std::vector<std::uint64_t> bounds(P + 1, 0);
-    {
-        std::vector<std::uint64_t> cuts;
-        L.upper_bounds(spl, cuts);
-        for (std::size_t j = 0; j + 1 < P; ++j) bounds[j + 1] = cuts[j];
-        bounds[P] = n;
-    }
-    // P x (P+1) matrix: row r = send counts of rank r to each dest, then its capacity
-    std::vector<std::uint64_t> row(P + 1), mat((P + 1) * P);
+    std::vector<std::uint64_t> bounds, recv_counts;
+    count_exchange<T>(comm, L, spl, n, L.capacity(), bounds, recv_counts);
+    // (the count allgather replaces the reference's piggybacked counts: not a collective of the
+    //  reference's accounting, so not counted in collective_ops)
+    std::vector<std::uint64_t> row(P);
     for (std::size_t d = 0; d < P; ++d) row[d] = bounds[d + 1] - bounds[d];
-    row[P] = L.capacity();
-    comm.allgather(row.data(), row.size() * sizeof(std::uint64_t), mat.data());
-    std::vector<std::uint64_t> recv_counts(P);
-    for (std::size_t s = 0; s < P; ++s) recv_counts[s] = mat[s * (P + 1) + me];
-    for (std::size_t r = 0; r < P; ++r) {
-        std::uint64_t need = 0;
-        for (std::size_t s = 0; s < P; ++s) need += mat[s * (P + 1) + r];
-        if (need > mat[r * (P + 1) + P]) {
-            std::uint64_t mine_need = 0;
-            for (std::size_t s = 0; s < P; ++s) mine_need += recv_counts[s];
-            throw proto_capacity_error("sihsort: output capacity too small on rank " + std::to_string(r),
-                                       mine_need);
-        }
-    }
     const bool tail = proto::tail_mode<T>(g.n);
     for (std::size_t d = 0; d < P; ++d) {
         if (d == me) continue;
@@ -415,6 +519,9 @@ void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_
     L.exchange(comm, bounds, recv_counts);
     st.output_count = L.merge_runs(bounds, recv_counts);  // local sort 2 of 2
     st.collective_ops = collectives;
+    for (std::uint64_t i = 0; i < collectives; ++i) comm.count_collective();
+    comm.ctr.p2p_sends += st.redistribution_sends;
+    comm.ctr.p2p_bytes += st.redistribution_bytes;
     if (splitters_out) *splitters_out = spl;
 }
 

@@ -29,13 +29,11 @@ __global__ void decompose_kernel(const std::uint64_t* __restrict__ comp, std::ui
         out[i] = static_cast<I>(comp[i] & 0xffffffffull);
 }
 
-int fast_env() {
-    static const int v = [] {
-        const char* e = std::getenv("AKB_SORTPERM_COMPOSITE");  // "0": stable onesweep over pairs
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
+// 0: stable onesweep over pairs (experiment builds: -DAKB_CFG_SORTPERM_COMPOSITE=0)
+#ifndef AKB_CFG_SORTPERM_COMPOSITE
+#define AKB_CFG_SORTPERM_COMPOSITE 1
+#endif
+constexpr int fast_env() { return AKB_CFG_SORTPERM_COMPOSITE; }
 
 }  // namespace
 

@@ -12,6 +12,7 @@
 #include <limits>
 #include <numeric>
 #include <random>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -289,6 +290,108 @@ void test_sihsort() {
 }
 
 
+void test_sihsort_stages() {  // SPEC.md:282-325 known answers for the stage functions
+    const std::vector<std::int64_t> ten{1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
+    CHECK(ak::sample_local<std::int64_t>(ten, 3) == (std::vector<std::int64_t>{1, 6, 10}));
+    CHECK(ak::sample_local<std::int64_t>(ten, 1) == (std::vector<std::int64_t>{6}));
+    CHECK(ak::sample_local<std::int64_t>(ten, 99).size() == 10);                              // k clamps to n
+    CHECK(ak::sample_local<std::int64_t>(std::span<const std::int64_t>{}, 4).empty());
+    const std::vector<std::int64_t> two{0, 10};
+    const auto h = ak::build_interpolated_histogram<std::int64_t>(two, 2);
+    CHECK(h.bin_edges == (std::vector<long double>{0.0L, 5.0L, 10.0L}));
+    CHECK(h.counts == (std::vector<std::uint64_t>{1, 1}));
+    CHECK(h.total == 2);
+    const auto deg = ak::build_interpolated_histogram<std::int64_t>(std::vector<std::int64_t>(5, 7), 4);
+    CHECK(deg.counts == (std::vector<std::uint64_t>{5}));  // degenerate range -> one bin
+    CHECK(ak::select_splitters<std::int64_t>(h, 2).values == (std::vector<std::int64_t>{5}));
+    CHECK(ak::select_splitters<std::int64_t>(h, 1).values.empty());
+    // redistribute: P=2, [1,2,9] / [3,8,10], splitter 5 -> rank0 [1,2,3], rank1 [9,8,10]
+    // (source-rank concatenation, not merged); a key equal to the splitter goes to
+    // the lower rank
+    {
+        ak::sim::world w(2);
+        std::vector<std::vector<std::int64_t>> out(2), tie(2);
+        ak::sim::run_ranks(w, [&](ak::sim::rank_comm& comm) {
+            const auto e = ak::exec_backend::cuda();
+            const auto r = comm.rank();
+            const std::vector<std::int64_t> mine = r == 0 ? std::vector<std::int64_t>{1, 2, 9}
+                                                          : std::vector<std::int64_t>{3, 8, 10};
+            out[r] = ak::redistribute<std::int64_t>(mine, ak::splitter_set<std::int64_t>{{5}}, comm, 6, e);
+            const std::vector<std::int64_t> t = r == 0 ? std::vector<std::int64_t>{5, 6} : std::vector<std::int64_t>{4, 5};
+            tie[r] = ak::redistribute<std::int64_t>(t, ak::splitter_set<std::int64_t>{{5}}, comm, 4, e);
+        });
+        CHECK(out[0] == (std::vector<std::int64_t>{1, 2, 3}));
+        CHECK(out[1] == (std::vector<std::int64_t>{9, 8, 10}));
+        CHECK(tie[0] == (std::vector<std::int64_t>{5, 4, 5}));
+        CHECK(tie[1] == (std::vector<std::int64_t>{6}));
+    }
+    // refine_splitters: a bad splitter on uniform data is corrected to a balanced one
+    {
+        const std::size_t P = 2, n = 100000;
+        ak::sim::world w(P);
+        std::vector<ak::refine_result<std::int64_t>> res(P);
+        ak::sim::run_ranks(w, [&](ak::sim::rank_comm& comm) {
+            const auto e = ak::exec_backend::cuda();
+            std::vector<std::int64_t> mine(n);
+            for (std::size_t i = 0; i < n; ++i) mine[i] = static_cast<std::int64_t>(i * P + comm.rank());
+            res[comm.rank()] = ak::refine_splitters<std::int64_t>(mine, ak::splitter_set<std::int64_t>{{10}}, comm,
+                                                                  ak::sih_config{}, e);
+        });
+        CHECK(res[0].converged && res[1].converged);
+        CHECK(res[0].splitters.values == res[1].splitters.values);
+        CHECK(res[0].rounds_used >= 2);
+        const auto s = res[0].splitters.values[0];
+        CHECK(s > 75000 && s < 125000);  // within imbalance_tol 0.25 of n_total / 2
+    }
+}
+
+void test_rank_comm() {  // sim_comm.hpp:84-181: messaging, values, all_reduce(merge), counters
+    const std::size_t P = 4;
+    ak::sim::world w(P);
+    std::vector<std::vector<std::int64_t>> got(P), red(P);
+    std::vector<ak::sim::rank_counters> ctr(P);
+    std::vector<std::string> err(P);
+    ak::sim::run_ranks(w, [&](ak::sim::rank_comm& comm) {
+        const auto e = ak::exec_backend::cuda();
+        const std::size_t r = comm.rank();
+        // ring of payload messages, then a control message back
+        const std::vector<std::int64_t> mine{static_cast<std::int64_t>(r), 10, 20};
+        comm.send_values<std::int64_t>((r + 1) % P, mine, ak::sim::traffic_class::payload, e);
+        got[r] = comm.recv_values<std::int64_t>((r + P - 1) % P, e);
+        const std::byte b[3] = {std::byte{1}, std::byte{2}, std::byte{3}};
+        comm.send((r + P - 1) % P, std::span<const std::byte>(b, 3), ak::sim::traffic_class::control, e);
+        const auto back = comm.recv((r + 1) % P, e);
+        if (back.size() != 3 || back[2] != std::byte{3}) err[r] = "control message";
+        // a 3-byte message cannot be read as int64 values (sim_comm.hpp:108-112)
+        comm.send((r + 1) % P, std::span<const std::byte>(b, 3), ak::sim::traffic_class::payload, e);
+        try {
+            (void)comm.recv_values<std::int64_t>((r + P - 1) % P, e);
+            err[r] = "no transport_error";
+        } catch (const ak::sim::transport_error&) {
+        }
+        // non-commutative merge: the reference's binomial tree order, identical on every rank
+        red[r] = comm.all_reduce(std::vector<std::int64_t>{static_cast<std::int64_t>(r + 1)},
+                                 [](std::vector<std::int64_t>& a, const std::vector<std::int64_t>& in) {
+                                     a[0] = a[0] * 10 + in[0];
+                                 },
+                                 e);
+        ctr[r] = comm.counters();
+    });
+    for (std::size_t r = 0; r < P; ++r) {
+        CHECK(err[r].empty());
+        CHECK(got[r] == (std::vector<std::int64_t>{static_cast<std::int64_t>((r + P - 1) % P), 10, 20}));
+        CHECK(red[r] == (std::vector<std::int64_t>{154}));  // ((1*10+3)*10 + (2*10+4))
+        CHECK(ctr[r].p2p_sends == 3);
+        CHECK(ctr[r].p2p_bytes == 24 + 3 + 3);
+        CHECK(ctr[r].collective_ops == 1);
+        CHECK(ctr[r].control_bytes_peak == 3);
+    }
+    CHECK(ctr[0].collective_sends == 2 && ctr[1].collective_sends == 2);  // binomial tree, P = 4
+    CHECK(ctr[2].collective_sends == 1 && ctr[3].collective_sends == 1);
+    CHECK_THROWS_AS(ak::sim::world(0), std::invalid_argument);
+    CHECK_THROWS_AS(ak::sim::world(2, 0), std::invalid_argument);
+}
+
 void test_predicates() {  // test_primitives.cpp:206-263 with comparison functors for the lambdas
     const std::vector<int> zeros(100, 0), ones(100, 1);
     for (auto algo : {ak::predicate_algo::early_exit, ak::predicate_algo::via_mapreduce}) {
@@ -366,7 +469,8 @@ int main() {
     const std::pair<const char*, void (*)()> tests[] = {
         {"partition", test_partition}, {"reduce", test_reduce},     {"accumulate", test_accumulate},
         {"search", test_search},       {"sort", test_sort},         {"sortperm", test_sortperm},
-        {"sihsort", test_sihsort},     {"predicates", test_predicates},
+        {"sihsort", test_sihsort},     {"sihsort_stages", test_sihsort_stages},
+        {"rank_comm", test_rank_comm}, {"predicates", test_predicates},
         {"distributed", test_distributed_reduce_scan}};
     for (const auto& [name, fn] : tests) {
         std::fprintf(stderr, "[ run ] %s\n", name);

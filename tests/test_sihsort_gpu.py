@@ -148,3 +148,24 @@ def test_sihsort_p8_large_properties(ak, dev):
     assert fingerprint(allin) == fingerprint(allout)
     assert max(o.numel() for o in outs) <= 1.25 * n
     assert all(s.converged == 1 for s in stats)
+
+
+@pytest.mark.parametrize("P,log2n,dt", [
+    (8, 22, np.int64), (8, 22, np.uint64), (2, 23, np.int64), (4, 23, np.int64),
+    (4, 24, np.uint64), (8, 25, np.int64), (2, 27, np.int64), (1, 28, np.int64)])
+def test_sihsort_at_scale_vs_live_reference(ak, orc, dev, P, log2n, dt):
+    """Per-rank outputs AND sih_stats bit-exact against the reference itself (oracle/_ref: the
+    unmodified /root/reference/proj sihsort over sim::world, all host threads) at sizes up to the
+    full config-4 per-GPU size (P=1 x 2^28) and 8 ranks x 2^25 (reference sihsort.hpp:508-569)."""
+    if not orc.ref_available():
+        pytest.skip("oracle/_ref not built")
+    import os
+    n = 1 << log2n
+    ins = [orc.ref_bench_keys(42, r, n, dt) for r in range(P)]
+    outs, stats = ak.sihsort_loopback([torch.from_numpy(a).to(dev) for a in ins])
+    want, wstats = orc.ref_sihsort(ins, threads_per_rank=max(1, (os.cpu_count() or 1) // P))
+    for r in range(P):
+        got = outs[r].cpu().numpy()
+        assert got.size == want[r].size, f"rank {r} size"
+        assert np.array_equal(got, want[r]), f"rank {r} output"
+        assert stats[r].as_dict() == wstats[r], f"rank {r} stats"
