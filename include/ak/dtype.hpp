@@ -2,8 +2,8 @@
 //
 // Codes 1-6 are the reference's and are part of the SIHS fixture format. This build sorts
 // i32/u32/i64/u64/f32/f64 on the device and adds two codes the reference lacks (SURVEY.md
-// §8(d) config 5 sorts UInt64): u64 = 7, u32 = 8. i16 and i128 keep their codes so fixture
-// headers written by the reference parse, but there is no device sort for them.
+// §8(d) config 5 sorts UInt64): u64 = 7, u32 = 8. i16 and i128 (codes 1 and 4) have the
+// device sort family (csrc/wide_keys.cu) but not sihsort / reduce / scan.
 #pragma once
 
 #include <cstddef>

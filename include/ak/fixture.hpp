@@ -1,8 +1,9 @@
 // ak/fixture.hpp -- SIHS per-rank input fixtures (reference proj/include/ak/fixture.hpp,
 // format of src/fixture.cpp:24-95), B200 build. Byte-identical layout, little-endian:
 // "SIHS" | version u32 (=1) | dtype code u32 | rank u32 | count u64 | count raw elements.
-// Files written by the reference read here and vice versa (tests/test_fixture.py checks
-// both directions against the reference compiled in place).
+// Codes 1-6 round-trip with the reference in both directions (tests/test_fixture_csv.py
+// checks both against the reference compiled in place). The u64 / u32 codes 7 and 8 are this
+// build's additions: the reference reader rejects them (it accepts codes 1-6 only).
 #pragma once
 
 #include <bit>

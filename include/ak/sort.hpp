@@ -1,8 +1,11 @@
 // ak/sort.hpp -- drop-in for proj/include/ak/sort.hpp (sort.hpp:22-290) on the B200 build.
 //
 // Same names, parameter orders, buffer structs and required_bytes, same exceptions thrown
-// before any mutation. The sort itself is libak_cuda.so's stable LSD onesweep radix sort
-// (identical output to the reference's stable merge sort: ties keep input order).
+// before any mutation. The sorts run in libak_cuda.so and give the reference's stable merge
+// sort's output exactly (ties keep input order): 64-bit integer keys-only sorts by the hybrid
+// MSD partition + on-chip counting stage (equal integer keys are indistinguishable, so any
+// correct order of them is the stable one), every other key type / payload sort by the
+// stable LSD onesweep radix sort.
 // Spans may live in host memory (staged through HBM, blocking) or in device memory
 // (sorted in place; device scratch spans are used as the radix ping-pong buffers).
 // Comparators: std::less<T> / std::less<> (ascending) and std::greater<T> / std::greater<>

@@ -1069,6 +1069,16 @@ struct lc_smem {
     static constexpr int MINB = total + 1024 <= 114 * 1024 ? 2 : 1;  // CTAs per SM that fit
 };
 
+// local_count3_kernel: as lc_smem plus a second counter table (the rank loop of range i still
+// reads its table while a faster warp zeroes the other one for range i + 1: no end barrier).
+template <typename T, int ITEMS>
+struct lc3_smem : lc_smem<T, ITEMS> {
+    using B = lc_smem<T, ITEMS>;
+    static constexpr std::size_t cnt2_off = B::total;
+    static constexpr std::size_t total = cnt2_off + B::cnt_bytes;
+    static constexpr int MINB = total + 1024 <= 114 * 1024 ? 2 : 1;
+};
+
 // The counting stage of one range whose keys are in registers (k[i] = key i*LC_BLOCK + tid;
 // padding repeats a valid key) and whose per-warp min / max partials of the ordered keys are
 // in s_red[0..15] / s_red[16..31] (written before the caller's barrier): bins, ranks, and stores key j of the sorted range to out[j]. Returns 1
@@ -1354,6 +1364,233 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
     }  // ranges
 }
 
+// Counting local stage, lean variant (TMA-fed input only): local_count_kernel's algorithm --
+// bins = the top nb varying bits (~2 bins per key), one shared atomic per key, keys staged in
+// bin order, then every staged position ranks its key inside its (short) bin and stores it to
+// its final place -- with the per-key instruction overhead cut: keys stay in ordered bits in
+// registers, varying bits = OR of key ^ first key (one 64-bit reduction instead of OR + AND),
+// no global-load fallback path (unaligned input takes local_count_kernel), 32-bit shared
+// addressing, 32-bit range loop, double-buffered reduction slots.
+// profiles/r02: local_count_kernel issued ~150 instructions per key (63% issue-busy, IPC 2.5).
+// Measured and dropped (r02): settling only the keys that share a bin (random in-bin reads +
+// an in-place rewrite) 2.10 ms, and coarse 16-key bins ranked by warp shuffles 5.2 ms, vs
+// 1.78 ms for the per-position rank below (at 2^28 int64).
+template <typename T, int ITEMS, bool DESC>
+__global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
+    local_count3_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
+                        std::uint64_t J, std::uint64_t* big, std::uint64_t* redo) {
+    using L = lc3_smem<T, ITEMS>;
+    using B = typename key_traits<T>::bits;
+    constexpr int CAP = L::CAP;
+    static_assert(sizeof(T) == 8, "8-byte keys");
+    constexpr B X = (std::is_signed_v<T> ? (B(1) << 63) : B(0)) ^ (DESC ? ~B(0) : B(0));  // raw <-> ordered
+    extern __shared__ __align__(16) unsigned char smem[];
+    B* s_red = reinterpret_cast<B*>(smem + L::red_off);  // [2][WARPS] OR partials
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    std::uint64_t* s_bar = reinterpret_cast<std::uint64_t*>(smem + L::bar_off);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto fits = [&](std::uint64_t rb, std::uint64_t re) {
+        return re > rb && re - rb <= static_cast<std::uint64_t>(CAP);
+    };
+    auto issue = [&](std::uint64_t r, int q) {  // one thread
+        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
+        if (!fits(rb, re)) return;
+        const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
+        const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
+        mbar_arrive_expect_tx(s_bar + q, bytes);
+        bulk_g2s(smem + L::buf_off + q * L::buf_bytes, in + a0, bytes, s_bar + q);
+    };
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        mbar_init(s_bar + 1, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    const std::uint32_t nr = static_cast<std::uint32_t>(J);  // ranges < 2^32 (n / 256 at most)
+    if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x, 0);
+    std::uint32_t phase = 0;  // bit q = parity of buffer q's next completion
+    const bool copy_equal = in != out;
+
+#pragma unroll 1
+    for (std::uint32_t r = blockIdx.x, it = 0; r < nr; r += gridDim.x, ++it) {
+        const int cur = static_cast<int>(it & 1);
+        const std::uint64_t b = cuts[r], e = cuts[r + 1];
+        const bool ok_range = fits(b, e);
+        const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
+        B* sb = reinterpret_cast<B*>(smem + L::buf_off + cur * L::buf_bytes) + static_cast<std::uint32_t>(b & 1);
+        B* red = s_red + cur * LC_WARPS;
+        // packed u16 counts / starts, one table per parity of the range
+        std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + (cur ? L::cnt2_off : L::cnt_off));
+        const std::uint16_t* s_c16 = reinterpret_cast<const std::uint16_t*>(s_cw);
+        B k[ITEMS];
+        B orx = 0;
+        if (ok_range) {
+            mbar_wait(s_bar + cur, (phase >> cur) & 1u);
+            phase ^= 1u << cur;
+            const B k0 = sb[0];
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const std::uint32_t li = static_cast<std::uint32_t>(i * LC_BLOCK + tid);
+                const B v = li < len ? sb[li] : k0;  // padding repeats key 0 (neutral below)
+                orx |= v ^ k0;
+                k[i] = v ^ X;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) orx |= __shfl_xor_sync(FULL, orx, o);
+        if (lane == 0) red[warp] = orx;
+        const int nb_want = min(LC_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
+        const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
+        if (nwords_w >= 4) {
+            for (int i = tid; i < nwords_w / 4; i += LC_BLOCK)
+                reinterpret_cast<uint4*>(s_cw)[i] = make_uint4(0, 0, 0, 0);
+        } else if (tid < nwords_w) {
+            s_cw[tid] = 0;
+        }
+        fence_proxy_async_smem();  // generic accesses to the other buffer precede its next TMA write
+        __syncthreads();
+        if (tid == 0 && r + gridDim.x < nr) issue(r + gridDim.x, cur ^ 1);
+        if (!ok_range) {
+            if (e - b > static_cast<std::uint64_t>(CAP) && tid == 0) {  // left for the segment fallback
+                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+                big[1 + slot] = r;
+            }
+            continue;
+        }
+        B vary = lane < LC_WARPS ? red[lane] : B(0);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
+        vary = __shfl_sync(FULL, vary, 0);
+        if (vary == 0) {  // every key equal: the range is already sorted
+            if (copy_equal)
+                for (std::uint32_t j = tid; j < len; j += LC_BLOCK) out[b + j] = static_cast<T>(k[0] ^ X);
+            continue;
+        }
+        const int hb = 63 - __clzll(static_cast<long long>(vary));
+        const int nb = max(1, min(nb_want, hb + 1));
+        const int shift = hb + 1 - nb;
+        const std::uint32_t bmask = (1u << nb) - 1u;
+        const std::uint32_t nwords = 1u << (nb - 1);
+
+        // ---- counting: one shared atomic per key on its bin's half word -> slot in the bin ----
+        // slots (< LC_MAX_BIN = 48: 6 bits) packed five per word; bins are recomputed from the keys
+        constexpr int SW = (ITEMS + 4) / 5;
+        std::uint32_t sl[SW];
+#pragma unroll
+        for (int w = 0; w < SW; ++w) sl[w] = 0;
+        bool over = false;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const bool ok = static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len;
+            const std::uint32_t bn = static_cast<std::uint32_t>(k[i] >> shift) & bmask;
+            const std::uint32_t sh = (bn & 1u) << 4;
+            const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
+            const std::uint32_t slot = (old >> sh) & 0xffffu;
+            over |= ok && slot >= LC_MAX_BIN;
+            sl[i / 5] |= (slot & 0x3fu) << (6 * (i % 5));
+        }
+        if (__syncthreads_or(over)) {  // clustered keys: the stable radix kernel takes the range
+            if (tid == 0) {
+                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(redo), 1ull);
+                redo[1 + slot] = r;
+            }
+            continue;
+        }
+        // ---- exclusive scan of the packed counts -> packed u16 bin starts (as local_count) ----
+        {
+            const std::uint32_t wpw = nwords / LC_WARPS;
+            const std::uint32_t nq = wpw / 128;
+            std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
+            if (nq >= 1) {
+                uint4 u[2];
+                std::uint32_t cs[2] = {0, 0};
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (q < static_cast<int>(nq)) {
+                        u[q] = *reinterpret_cast<const uint4*>(wbase + q * 128);
+                        const std::uint32_t S = u[q].x + u[q].y + u[q].z + u[q].w;
+                        cs[q] = (S & 0xffffu) + (S >> 16);
+                    }
+                std::uint32_t p = cs[0] | (cs[1] << 16);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const std::uint32_t y = __shfl_up_sync(FULL, p, o);
+                    if (lane >= o) p += y;
+                }
+                const std::uint32_t t = __shfl_sync(FULL, p, 31);
+                const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
+                if (lane == 0) s_wsum[warp] = T0 + T1;
+                __syncthreads();
+                std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
+                const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (q < static_cast<int>(nq)) {
+                        std::uint32_t run = exq[q];
+                        std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u[q]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
+                            wv[j] = run | ((run + lo) << 16);
+                            run += lo + hi;
+                        }
+                        *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
+                    }
+            } else {
+                const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
+                const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
+                const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
+                const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
+                const std::uint32_t S = c0 + c1;
+                const std::uint32_t sum = (S & 0xffffu) + (S >> 16);
+                std::uint32_t inc = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                if (lane == 31) s_wsum[warp] = inc;
+                __syncthreads();
+                std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
+                std::uint32_t run = wp + inc - sum;
+                if (w0 < nwords) {
+                    const std::uint32_t lo = c0 & 0xffffu, hi = c0 >> 16;
+                    s_cw[w0] = run | ((run + lo) << 16);
+                    run += lo + hi;
+                }
+                if (wpt == 2 && w0 + 1 < nwords) s_cw[w0 + 1] = run | ((run + (c1 & 0xffffu)) << 16);
+            }
+            if (tid == 0) reinterpret_cast<std::uint16_t*>(s_cw)[2 * nwords] = static_cast<std::uint16_t>(len);
+        }
+        __syncthreads();
+        // ---- keys into bin order (the range's own TMA buffer is free: keys are in registers) ----
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i)
+            if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len)
+                sb[s_c16[static_cast<std::uint32_t>(k[i] >> shift) & bmask] + ((sl[i / 5] >> (6 * (i % 5))) & 0x3fu)] = k[i];
+        __syncthreads();
+        // ---- each position ranks its key inside its bin: final slot = bin start + #(key, pos) smaller ----
+        T* o = out + b;
+#pragma unroll 1
+        for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
+            const B v = sb[x];
+            const std::uint32_t bn = static_cast<std::uint32_t>(v >> shift) & bmask;
+            const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
+            std::uint32_t rk = x;
+            if (cnt > 1) {
+                rk = st + lex_less96(sb[st], st, v, x) + lex_less96(sb[st + 1], st + 1, v, x);
+#pragma unroll 1
+                for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(sb[y], y, v, x);
+            }
+            o[rk] = static_cast<T>(v ^ X);
+        }
+    }  // ranges
+}
+
 // cut j = first index of the bucket (top bits) holding position j*step; cuts[J] = n.
 template <typename T>
 __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
@@ -1596,16 +1833,22 @@ void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cut
     static_assert(CITEMS * LC_BLOCK == ITEMS * LOCAL_BLOCK, "same range capacity");
     using CS = lc_smem<T, CITEMS>;
     using LS = local_smem<T, ITEMS>;
-    smem_attr(c, local_count_kernel<T, CITEMS, false>, CS::total);
-    smem_attr(c, local_count_kernel<T, CITEMS, true>, CS::total);
     smem_attr(c, local_redo_kernel<T, ITEMS>, LS::total);
     AKB_CUDA(cudaMemsetAsync(redo, 0, sizeof(std::uint64_t), c->stream));
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * CS::MINB));
-    if (desc)
-        local_count_kernel<T, CITEMS, true><<<grid, LC_BLOCK, CS::total, c->stream>>>(G, kout, cuts, J, big, redo);
-    else
-        local_count_kernel<T, CITEMS, false><<<grid, LC_BLOCK, CS::total, c->stream>>>(G, kout, cuts, J, big, redo);
+    if ((reinterpret_cast<std::uintptr_t>(G) & 15) == 0) {  // TMA-fed lean kernel
+        using C3 = lc3_smem<T, CITEMS>;
+        const unsigned grid3 =
+            static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * C3::MINB));
+        auto kern = desc ? local_count3_kernel<T, CITEMS, true> : local_count3_kernel<T, CITEMS, false>;
+        smem_attr(c, kern, C3::total);
+        kern<<<grid3, LC_BLOCK, C3::total, c->stream>>>(G, kout, cuts, J, big, redo);
+    } else {
+        auto kern = desc ? local_count_kernel<T, CITEMS, true> : local_count_kernel<T, CITEMS, false>;
+        smem_attr(c, kern, CS::total);
+        kern<<<grid, LC_BLOCK, CS::total, c->stream>>>(G, kout, cuts, J, big, redo);
+    }
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     local_redo_kernel<T, ITEMS><<<static_cast<unsigned>(c->sm_count * 2), LOCAL_BLOCK, LS::total, c->stream>>>(

@@ -106,7 +106,7 @@ def test_accumulate_minmax(ak, ex, dev):
 @pytest.mark.parametrize("dt", [np.int32, np.int64, np.uint64, np.float64])
 @pytest.mark.parametrize("n", [(1 << 23), (1 << 23) + 12345])
 def test_accumulate_persistent_path(ak, orc, ex, dev, dt, n):
-    """Sizes past 4 x SM-count tiles take the persistent TMA-fed scan (scan_persist_kernel):
+    """Large sizes (hundreds of 32 KB tiles in flight across the SMs, long look-back chains):
     inclusive, exclusive and in-place (x is out) sums, and running max, exact vs the oracle."""
     x = vals(np.random.default_rng(n + 7), dt, n)
     for inclusive in (True, False):
@@ -175,3 +175,15 @@ def test_searchsorted_matches_oracle(ak, orc, ex, dev, dt):
     for side in ("first", "last"):
         got = ak.searchsorted(t(hay, dev), t(nd, dev), side, ex).cpu().numpy().astype(np.uint64)
         assert np.array_equal(got, orc.searchsorted(hay, nd, side))
+
+
+def test_reduce_non_identity_init_folds_once(ak, orc, ex, dev):
+    """Documented deviation: init is folded exactly once. The reference folds
+    it per worker chunk and once more (reduce.hpp:31-56): 1000 ones with init 100 give 1200 on its
+    sequential backend and 1300 on 2 threads; this build gives 1100 on every launch shape."""
+    x = np.ones(1000, dtype=np.int64)
+    assert ak.reduce("sum", torch.from_numpy(x).to(dev), 100, ex) == 1100
+    assert ak.reduce("sum", torch.from_numpy(np.ones(1 << 22, dtype=np.int64)).to(dev), 100, ex) == (1 << 22) + 100
+    if orc.ref_available():
+        assert orc.ref_reduce(x, init=100, threads=0) == 1200
+        assert orc.ref_reduce(x, init=100, threads=2) == 1300

@@ -5,6 +5,8 @@
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/cub_yardstick.cu -o build/cub_yardstick
 //   build/cub_yardstick [log2n=28]
+// Every CUB call's status is checked (r01's run printed 0.003 ms for SortKeys: the call had
+// failed on a 64-bit item count and nothing noticed). Item counts are passed as int (n < 2^31).
 #include <cub/cub.cuh>
 
 #include <cstdio>
@@ -46,6 +48,11 @@ float time_ms(F&& f, int reps = 5) {
 int main(int argc, char** argv) {
     const int lg = argc > 1 ? std::atoi(argv[1]) : 28;
     const size_t n = size_t(1) << lg;
+    if (lg > 30) {
+        std::fprintf(stderr, "log2n <= 30\n");
+        return 2;
+    }
+    const int ni = static_cast<int>(n);
     std::vector<int64_t> h(n);
     std::mt19937_64 rng(42);
     for (auto& v : h) v = static_cast<int64_t>(rng());
@@ -55,24 +62,34 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(k0, h.data(), n * 8, cudaMemcpyHostToDevice));
     void* tmp = nullptr;
     size_t tb = 0;
-    cub::DeviceRadixSort::SortKeys(tmp, tb, k0, k1, n);
+    CK(cub::DeviceRadixSort::SortKeys(tmp, tb, k0, k1, ni));
     size_t tb2 = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, tb2, k0, k1, n);
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb2, k0, k1, ni));
     tb = std::max(tb, tb2) + (size_t(1) << 20);
     CK(cudaMalloc(&tmp, tb));
     float ms = time_ms([&] {
         size_t t = tb;
-        cub::DeviceRadixSort::SortKeys(tmp, t, k0, k1, n);
+        CK(cub::DeviceRadixSort::SortKeys(tmp, t, k0, k1, ni));
     });
-    std::printf("cub SortKeys int64 n=2^%d: %.3f ms  (%.1f GB/s keys)\n", lg, ms, n * 8 / 1e6 / ms);
+    {
+        std::vector<int64_t> o(n);
+        CK(cudaMemcpy(o.data(), k1, n * 8, cudaMemcpyDeviceToHost));
+        for (size_t i = 1; i < n; ++i)
+            if (o[i - 1] > o[i]) {
+                std::fprintf(stderr, "cub SortKeys output not sorted at %zu\n", i);
+                return 1;
+            }
+    }
+    std::printf("cub SortKeys int64 n=2^%d: %.3f ms  (%.1f GB/s keys, output checked sorted)\n", lg, ms,
+                n * 8 / 1e6 / ms);
     ms = time_ms([&] {
         size_t t = tb;
-        cub::DeviceScan::InclusiveSum(tmp, t, k0, k1, n);
+        CK(cub::DeviceScan::InclusiveSum(tmp, t, k0, k1, ni));
     });
     std::printf("cub InclusiveSum int64 n=2^%d: %.3f ms  (%.1f GB/s r+w)\n", lg, ms, n * 16 / 1e6 / ms);
     ms = time_ms([&] {
         size_t t = tb;
-        cub::DeviceReduce::Sum(tmp, t, k0, k1, n);
+        CK(cub::DeviceReduce::Sum(tmp, t, k0, k1, ni));
     });
     std::printf("cub Reduce int64 n=2^%d: %.3f ms  (%.1f GB/s)\n", lg, ms, n * 8 / 1e6 / ms);
     // f32 keys + i32 payload (config 2 shape at n)
@@ -85,7 +102,7 @@ int main(int argc, char** argv) {
     for (auto& v : hf) v = U(rng);
     CK(cudaMemcpy(f0, hf.data(), n * 4, cudaMemcpyHostToDevice));
     size_t tb3 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb3, f0, f1, v0, v1, n);
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb3, f0, f1, v0, v1, ni));
     if (tb3 > tb) {
         CK(cudaFree(tmp));
         tb = tb3;
@@ -93,13 +110,13 @@ int main(int argc, char** argv) {
     }
     ms = time_ms([&] {
         size_t t = tb;
-        cub::DeviceRadixSort::SortPairs(tmp, t, f0, f1, v0, v1, n);
+        CK(cub::DeviceRadixSort::SortPairs(tmp, t, f0, f1, v0, v1, ni));
     });
     std::printf("cub SortPairs f32/i32 n=2^%d: %.3f ms\n", lg, ms);
     float* g = reinterpret_cast<float*>(k1);
     ms = time_ms([&] {
         size_t t = tb;
-        cub::DeviceScan::InclusiveSum(tmp, t, f0, g, n);
+        CK(cub::DeviceScan::InclusiveSum(tmp, t, f0, g, ni));
     });
     std::printf("cub InclusiveSum f32 n=2^%d: %.3f ms  (%.1f GB/s r+w)\n", lg, ms, n * 8 / 1e6 / ms);
     return 0;
