@@ -123,10 +123,17 @@ def _check(rc: int, extra_required: int | None = None) -> None:
     raise RuntimeError(f"ak error {rc}: {msg}")
 
 
+_FN_CACHE: dict = {}
+
+
 def _fn(name: str, argtypes, restype=C.c_int):
-    f = getattr(_lib, name)
-    f.argtypes = argtypes
-    f.restype = restype
+    """The C-ABI symbol with its prototype set (once per symbol: one signature per name)."""
+    f = _FN_CACHE.get(name)
+    if f is None:
+        f = getattr(_lib, name)
+        f.argtypes = argtypes
+        f.restype = restype
+        _FN_CACHE[name] = f
     return f
 
 

@@ -575,6 +575,8 @@ int ak_ctx_destroy(ak_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
+        for (auto& g : c->graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
         if (c->aux) cudaFree(c->aux);
         if (c->lookback) cudaFree(c->lookback);
         if (c->scan_flags) cudaFree(c->scan_flags);

@@ -73,6 +73,22 @@ struct ak_ctx {
     // counters (reported by ak_ctx_stats)
     std::uint64_t kernel_launches = 0;
 
+    // small keys-only sorts replayed as CUDA graphs (one launch), keyed by their buffers
+    struct small_graph {
+        const void* kin = nullptr;
+        void* kout = nullptr;
+        void* kalt = nullptr;
+        std::uint64_t n = 0;
+        int desc = 0;
+        int width = 0;
+        const void* cuts = nullptr;
+        const void* pinned = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        std::uint64_t launches = 0;
+    };
+    std::vector<small_graph> graphs;  // most recent last, at most 4
+    small_graph last_small;           // key of the last eager run (captured on a repeat)
+
     // optional per-kernel-family timing with CUDA events on the launch stream
     int profiling = 0;
     struct timed {

@@ -203,10 +203,12 @@ struct mp_smem {
     static constexpr std::size_t total = misc_off + 16;
 };
 
+// LEVEL 0: one 8-bit digit chosen on the device (plan = {mode, shift}: mode != 0 -> no-op),
+// cursors = that digit's exclusive offsets (small keys-only sorts, no host round trip).
 template <typename T, int LEVEL>
 __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     msd_pass_kernel(const T* __restrict__ in, T* __restrict__ out, std::uint64_t n, int desc,
-                    std::uint64_t* __restrict__ cursors) {
+                    std::uint64_t* __restrict__ cursors, const int* __restrict__ plan = nullptr) {
     using L = mp_smem;
     extern __shared__ __align__(16) unsigned char smem[];
     T* s_stage = reinterpret_cast<T*>(smem + L::stage_off);
@@ -222,7 +224,11 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL L > 1 = the 8L-bit prefixes
     // of the (already 8(L-1)-bit partitioned) tile, relative to its first key's 8(L-1)-bit
     // prefix (cursor index = the 8L-bit prefix)
-    constexpr int TOP = 64 - 8 * LEVEL;  // shift of the 8L-bit prefix
+    if constexpr (LEVEL == 0) {
+        if (plan[0] != 0) return;
+    }
+    const int TOP = LEVEL == 0 ? plan[1] : 64 - 8 * LEVEL;  // shift of the 8L-bit prefix (digit)
+    constexpr std::uint32_t DMASK = LEVEL == 0 ? 0xffu : 0xffffffffu;
     std::uint32_t lo16 = 0, span = 1;
     if (LEVEL >= 2) {
         const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> (TOP + 8));
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
         lo16 = f << 8;
         span = l - f + 1;
     }
-    const std::uint32_t nbins = LEVEL == 1 ? 256u : 256u * span;
+    const std::uint32_t nbins = LEVEL <= 1 ? 256u : 256u * span;
     if (LEVEL >= 2 && span > MP_SPAN) {
         // tiny buckets (skewed keys): per-key cursor claims, written straight out
         for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
@@ -266,7 +272,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     auto item_ok = [&](int i) { return 2 * ((i / 2) * MP_BLOCK + tid) + (i & 1) < static_cast<int>(len); };
     auto bin_of = [&](T key) {
         const std::uint64_t o = ord64(key, dsc);
-        return static_cast<std::uint32_t>(o >> TOP) - lo16;
+        return (static_cast<std::uint32_t>(o >> TOP) & DMASK) - lo16;
     };
     __syncthreads();
     // slots inside the bins (arbitrary order): one shared atomic per key
@@ -495,6 +501,18 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
 }
 
 template <typename T>
+void msd_digit_pass(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc, std::uint64_t* cursors,
+                    const int* plan) {
+    smem_attr(c, msd_pass_kernel<T, 0>, mp_smem::total);
+    const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
+    const int tok = ctx_prof_begin(c, KF_MSD);
+    msd_pass_kernel<T, 0><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kout, n, desc ? 1 : 0, cursors, plan);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 1;
+}
+
+template <typename T>
 void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc) {
     smem_attr(c, msd_pass_kernel<T, 3>, mp_smem::total);
     std::uint64_t* cur24 = ctx_msd3(c);                                   // 2^24 u64 cursors
@@ -551,6 +569,10 @@ std::uint64_t msd_max_bucket(ak_ctx* c, int level) {
     return *h;
 }
 
+template void msd_digit_pass<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::uint64_t, bool,
+                                           std::uint64_t*, const int*);
+template void msd_digit_pass<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t, bool,
+                                            std::uint64_t*, const int*);
 template void msd_level3<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::uint64_t, bool);
 template void msd_level3<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t, bool);
 template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t, bool, std::uint64_t*,

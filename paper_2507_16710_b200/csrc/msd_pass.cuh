@@ -28,6 +28,12 @@ void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool 
 template <typename T>
 void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc);
 
+// One unstable partition pass by the 8-bit digit at plan[1] (device plan, no-op when
+// plan[0] != 0); cursors = the digit's exclusive offsets (consumed).
+template <typename T>
+void msd_digit_pass(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc, std::uint64_t* cursors,
+                    const int* plan);
+
 // Largest bucket after the MSD levels (level 2: 16-bit buckets, 3: 24-bit), on the host.
 std::uint64_t msd_max_bucket(ak_ctx* c, int level);
 

@@ -309,7 +309,13 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     onesweep_kernel(const T* __restrict__ kin, T* __restrict__ kout, const V* __restrict__ vin,
                     V* __restrict__ vout, std::uint64_t n, int shift, int desc, int pass_index,
                     const std::uint64_t* __restrict__ goffs, std::uint64_t* lookback,
-                    std::uint32_t* tile_counter, std::uint32_t tag, int write_keys) {
+                    std::uint32_t* tile_counter, std::uint32_t tag, int write_keys,
+                    const int* __restrict__ plan) {
+    // device-planned pass (small keys-only sorts): plan[0] != 0 = not applicable, plan[1] = shift
+    if (plan != nullptr) {
+        if (plan[0] != 0) return;
+        shift = plan[1];
+    }
     using L = pass_smem<T, V, MODE>;
     constexpr int BLOCK = L::BLOCK;
     constexpr int ITEMS = tile_cfg<T, V, MODE>::ITEMS;
@@ -648,7 +654,7 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
 template <typename T, typename V, int MODE, int HW>
 void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift,
                       bool desc, int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter,
-                      bool write_keys) {
+                      bool write_keys, const int* plan = nullptr) {
     using L = pass_smem<T, V, MODE>;
     auto kern = onesweep_kernel<T, V, MODE, HW>;
     smem_attr(c, kern, L::total);
@@ -657,7 +663,7 @@ void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, s
     const int tok = ctx_prof_begin(c, KF_ONESWEEP);
     kern<<<static_cast<unsigned>(tiles), L::BLOCK, L::total, c->stream>>>(
         kin, kout, vin, vout, n, shift, desc ? 1 : 0, pass_index, goffs, c->lookback, tile_counter, tag,
-        write_keys ? 1 : 0);
+        write_keys ? 1 : 0, plan);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     c->kernel_launches += 1;
@@ -665,9 +671,10 @@ void launch_pass_impl(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, s
 
 template <typename T, typename V, int MODE>
 void launch_pass(ak_ctx* c, const T* kin, T* kout, const V* vin, V* vout, std::uint64_t n, int shift, bool desc,
-                 int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter, bool write_keys) {
+                 int pass_index, const std::uint64_t* goffs, std::uint32_t* tile_counter, bool write_keys,
+                 const int* plan = nullptr) {
     launch_pass_impl<T, V, MODE, AKB_CFG_MATCH>(c, kin, kout, vin, vout, n, shift, desc, pass_index, goffs,
-                                                tile_counter, write_keys);
+                                                tile_counter, write_keys, plan);
 }
 
 template <typename T, typename V, int MODE>
@@ -1591,6 +1598,67 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
     }  // ranges
 }
 
+// Device plan of a small keys-only sort (no host round trip): among the top three digits
+// (histograms in g_hist), the highest one that is not constant partitions the keys into 256
+// buckets by one onesweep pass. Writes plan = {mode, shift} (mode 0 = go; 1 = its largest
+// bucket exceeds cap: the host plan takes over after the call's one synchronisation), that
+// digit's exclusive offsets (the pass's bucket starts) and the range cuts (the bucket
+// starts; all zero when mode != 0, so the local stage finds only empty ranges).
+__global__ void __launch_bounds__(RADIX) small_plan_kernel(const std::uint64_t* __restrict__ g_hist, std::uint64_t n,
+                                                           std::uint64_t cap, int* __restrict__ plan,
+                                                           std::uint64_t* __restrict__ offs,
+                                                           std::uint64_t* __restrict__ cuts,
+                                                           std::uint64_t* __restrict__ big,
+                                                           std::uint64_t* __restrict__ redo) {
+    __shared__ std::uint64_t s_w[RADIX / 32];
+    __shared__ int s_d;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) s_d = -1;
+    __syncthreads();
+    std::uint64_t mx = 0;
+    for (int d = 7; d >= 5; --d) {  // block-uniform loop
+        std::uint64_t m = g_hist[d * RADIX + t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const std::uint64_t y = __shfl_xor_sync(FULL, m, o);
+            m = m > y ? m : y;
+        }
+        if (lane == 0) s_w[w] = m;
+        __syncthreads();
+        mx = 0;
+        for (int i = 0; i < RADIX / 32; ++i) mx = mx > s_w[i] ? mx : s_w[i];
+        __syncthreads();
+        if (mx < n) {
+            if (t == 0) s_d = d;
+            break;
+        }
+    }
+    __syncthreads();
+    const int d = s_d;
+    const int mode = (d < 0 || mx > cap) ? 1 : 0;
+    const std::uint64_t v = d >= 0 ? g_hist[d * RADIX + t] : 0;
+    std::uint64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const std::uint64_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    std::uint64_t base = 0;
+    for (int i = 0; i < w; ++i) base += s_w[i];
+    const std::uint64_t ex = base + inc - v;
+    offs[t] = ex;
+    cuts[t] = mode == 0 ? ex : 0;
+    if (t == 0) {
+        cuts[RADIX] = mode == 0 ? n : 0;
+        plan[0] = mode;
+        plan[1] = 8 * (d < 0 ? 0 : d);
+        big[0] = 0;  // the local stage's oversized / clustered range lists
+        redo[0] = 0;
+    }
+}
+
 // cut j = first index of the bucket (top bits) holding position j*step; cuts[J] = n.
 template <typename T>
 __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, int top_shift, int desc,
@@ -1828,13 +1896,13 @@ constexpr int local_count_env() { return AKB_CFG_LOCAL_COUNT; }
 // it handed back (persistent loop over redo[1 .. redo[0]]; no host round trip).
 template <typename T, int ITEMS>
 void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, std::uint64_t n,
-                        bool desc, int low, std::uint64_t* big, std::uint64_t* redo) {
+                        bool desc, int low, std::uint64_t* big, std::uint64_t* redo, bool redo_zeroed = false) {
     constexpr int CITEMS = ITEMS * LOCAL_BLOCK / LC_BLOCK;
     static_assert(CITEMS * LC_BLOCK == ITEMS * LOCAL_BLOCK, "same range capacity");
     using CS = lc_smem<T, CITEMS>;
     using LS = local_smem<T, ITEMS>;
     smem_attr(c, local_redo_kernel<T, ITEMS>, LS::total);
-    AKB_CUDA(cudaMemsetAsync(redo, 0, sizeof(std::uint64_t), c->stream));
+    if (!redo_zeroed) AKB_CUDA(cudaMemsetAsync(redo, 0, sizeof(std::uint64_t), c->stream));
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * CS::MINB));
     if ((reinterpret_cast<std::uintptr_t>(G) & 15) == 0) {  // TMA-fed lean kernel
@@ -1865,10 +1933,125 @@ void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cut
 // n * prod(max bin / n) (exact for m = 1, independence otherwise), and the smallest m whose
 // buckets fit a CTA is taken. Skewed inputs thus get more global digits instead of
 // oversized ranges; a mis-estimate only costs the (bounded) segment fallback.
+// Ranges the local stage left in `big` (oversized buckets of skewed keys): plain LSD on each
+// segment, or on the whole array when there are many. Needs the big count on the host.
+template <typename T>
+void sort_oversized(ak_ctx* c, const T* G, T* kout, T* kalt, std::uint64_t n, bool desc, const std::uint64_t* cuts,
+                    const std::uint64_t* big, std::uint64_t J, std::uint64_t nbig) {
+    if (!nbig) return;
+    std::vector<std::uint64_t> hc(J + 1), hl(nbig);
+    AKB_CUDA(cudaMemcpy(hc.data(), cuts, (J + 1) * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+    AKB_CUDA(cudaMemcpy(hl.data(), big + 1, nbig * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+    const bool whole = nbig > 32;
+    for (std::uint64_t r : hl) {
+        const std::uint64_t b = hc[r], len = hc[r + 1] - hc[r];
+        if (G != kout) AKB_CUDA(cudaMemcpyAsync(kout + b, G + b, len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+        if (whole) continue;
+        T* scratch = (G == kout) ? kalt + b : const_cast<T*>(G) + b;
+        radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout + b, kout + b, scratch, nullptr, nullptr, nullptr, len,
+                                                     desc, true);
+    }
+    if (whole) {
+        T* scratch = (G == kout) ? kalt : const_cast<T*>(G);
+        radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout, kout, scratch, nullptr, nullptr, nullptr, n, desc, true);
+    }
+}
+
+constexpr std::uint64_t SMALL_DEVICE_MAX = std::uint64_t(1) << 21;  // device-planned path up to here
+
+// Small keys-only 64-bit integer sorts with NO host round trip before the last kernel: the top
+// three digits' histograms -> device plan (small_plan_kernel) -> one unstable partition pass
+// by the chosen digit (msd_pass_kernel<0>: per-bin atomic cursors, no look-back state) ->
+// bucket cuts = its offsets -> counting local stage. The sequence is replayed as one CUDA
+// graph once the same buffers come back (every launch parameter lives in the ctx), and the
+// call's only synchronisation at the end reads {plan mode, oversized-range count}; only
+// skewed inputs then take the host-planned path. Returns false when that path must run.
+template <typename T>
+bool small_sort_device(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
+    constexpr int PASSES = 8;
+    constexpr int ITEMS = 12;  // 4608-key ranges, two counting CTAs per SM
+    constexpr std::uint64_t CAPK = LC_BLOCK * (ITEMS * LOCAL_BLOCK / LC_BLOCK);
+    std::uint64_t* g_hist = static_cast<std::uint64_t*>(c->small);  // rows 5..7 used
+    std::uint64_t* curs = g_hist + PASSES * RADIX;  // the chosen digit's offsets: the partition's cursors
+    const std::uint64_t J = RADIX;
+    // [cuts J+1][plan {mode, shift}][big count + list J][redo count + list J]: plan and the big
+    // count are adjacent, so one 16-byte read back gives both
+    std::uint64_t* cuts = ctx_cuts(c, 3 * J + 6);
+    int* plan = reinterpret_cast<int*>(cuts + J + 1);
+    std::uint64_t* big = cuts + J + 2;
+    std::uint64_t* redo = big + J + 1;
+    auto* h = static_cast<std::uint64_t*>(ctx_pinned(c, 2 * sizeof(std::uint64_t)));
+    // few, fat histogram CTAs: each flushes 3 x 256 global atomics, which dominate at small n
+    const unsigned hist_grid = static_cast<unsigned>(
+        std::max<std::uint64_t>(1, std::min<std::uint64_t>(static_cast<std::uint64_t>(c->sm_count) * 4,
+                                                            ceil_div(n, 256 * 64))));
+    auto enqueue = [&] {
+        AKB_CUDA(cudaMemsetAsync(g_hist + (PASSES - 3) * RADIX, 0, 3 * RADIX * sizeof(std::uint64_t), c->stream));
+        const int tok = ctx_prof_begin(c, KF_HIST);
+        hist_kernel<T, PASSES, PASSES - 3><<<hist_grid, 256, 0, c->stream>>>(kin, n, desc ? 1 : 0, g_hist);
+        AKB_CUDA(cudaGetLastError());
+        ctx_prof_end(c, tok);
+        small_plan_kernel<<<1, RADIX, 0, c->stream>>>(g_hist, n, CAPK - 64, plan, curs, cuts, big, redo);
+        AKB_CUDA(cudaGetLastError());
+        msd_digit_pass<T>(c, kin, kalt, n, desc, curs, plan);
+        launch_local_count<T, ITEMS>(c, kalt, kout, cuts, J, n, desc, 0, big, redo, true);
+        c->kernel_launches += 2;
+        AKB_CUDA(cudaMemcpyAsync(h, plan, 2 * sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    };
+    const ak_ctx::small_graph key{kin, kout, kalt, n, desc ? 1 : 0, static_cast<int>(sizeof(T)), cuts, h, nullptr, 0};
+    auto same = [&](const ak_ctx::small_graph& g) {
+        return g.kin == key.kin && g.kout == key.kout && g.kalt == key.kalt && g.n == key.n && g.desc == key.desc &&
+               g.width == key.width && g.cuts == key.cuts && g.pinned == key.pinned;
+    };
+    cudaGraphExec_t exec = nullptr;
+    if (!c->profiling) {
+        for (auto& g : c->graphs)
+            if (same(g)) {
+                exec = g.exec;
+                c->kernel_launches += g.launches;
+            }
+        if (!exec && same(c->last_small)) {  // the same buffers again: capture once, replay from now on
+            const std::uint64_t before = c->kernel_launches;
+            cudaGraph_t graph = nullptr;
+            AKB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue();
+            } catch (...) {
+                cudaStreamEndCapture(c->stream, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            AKB_CUDA(cudaStreamEndCapture(c->stream, &graph));
+            AKB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+            AKB_CUDA(cudaGraphDestroy(graph));
+            ak_ctx::small_graph g = key;
+            g.exec = exec;
+            g.launches = c->kernel_launches - before;
+            if (c->graphs.size() >= 4) {
+                AKB_CUDA(cudaGraphExecDestroy(c->graphs.front().exec));
+                c->graphs.erase(c->graphs.begin());
+            }
+            c->graphs.push_back(g);
+        }
+    }
+    if (exec) AKB_CUDA(cudaGraphLaunch(exec, c->stream));
+    else enqueue();
+    c->last_small = key;
+    AKB_CUDA(cudaStreamSynchronize(c->stream));  // the call's one synchronisation
+    const int mode = static_cast<int>(h[0] & 0xffffffffu);
+    const std::uint64_t nbig = h[1];
+    if (mode != 0) return false;  // nothing was written: the host plan starts from kin
+    sort_oversized<T>(c, kalt, kout, kalt, n, desc, cuts, big, J, nbig);
+    return true;
+}
+
 template <typename T>
 bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
     constexpr int PASSES = key_traits<T>::nbits / 8;
     const int env = hybrid_env();
+    if (env < 0 && c->blocking && n > static_cast<std::uint64_t>(LOCAL_TILE) && n <= SMALL_DEVICE_MAX &&
+        ((reinterpret_cast<std::uintptr_t>(kalt) & 15) == 0) && small_sort_device<T>(c, kin, kout, kalt, n, desc))
+        return true;
     // 64-bit integer keys. Float keys concentrate their top digits in the exponent (uniform
     // floats of [-1e6, 1e6) use ~40 of 256 top-digit values), which breaks the bucket-size
     // estimate and sends most ranges to the fallback (measured r01: f32 2^27 6.6 ms hybrid
@@ -2066,27 +2249,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     std::uint64_t* hb = static_cast<std::uint64_t*>(ctx_pinned(c, sizeof(std::uint64_t)));
     AKB_CUDA(cudaMemcpyAsync(hb, big, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
     AKB_CUDA(cudaStreamSynchronize(c->stream));
-    const std::uint64_t nbig = hb[0];
-    if (nbig) {
-        std::vector<std::uint64_t> hc(J + 1), hl(nbig);
-        AKB_CUDA(cudaMemcpy(hc.data(), cuts, (J + 1) * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
-        AKB_CUDA(cudaMemcpy(hl.data(), big + 1, nbig * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
-        const bool whole = nbig > 32;
-        for (std::uint64_t r : hl) {
-            const std::uint64_t b = hc[r], len = hc[r + 1] - hc[r];
-            if (G != kout)
-                AKB_CUDA(cudaMemcpyAsync(kout + b, G + b, len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
-            if (whole) continue;
-            T* scratch = (G == kout) ? kalt + b : const_cast<T*>(G) + b;
-            radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout + b, kout + b, scratch, nullptr, nullptr, nullptr,
-                                                         len, desc, true);
-        }
-        if (whole) {
-            T* scratch = (G == kout) ? kalt : const_cast<T*>(G);
-            radix_sort_impl<T, std::uint32_t, SORT_KEYS>(c, kout, kout, scratch, nullptr, nullptr, nullptr, n, desc,
-                                                         true);
-        }
-    }
+    sort_oversized<T>(c, G, kout, kalt, n, desc, cuts, big, J, hb[0]);
     return true;
 }
 

@@ -131,3 +131,20 @@ def test_msd_path_uint64_out_of_place(ak, ex, dev):
     y = ak.merge_sort_copy(d, ex=ex, cmp="greater")
     assert np.array_equal(d.cpu().numpy().view(np.uint64), x)
     assert np.array_equal(y.cpu().numpy().view(np.uint64), np.sort(x)[::-1])
+
+
+@pytest.mark.parametrize("n", [50_000, 1_000_000, 2_000_000])
+def test_small_sort_graph_replays(ak, ex, dev, n):
+    """Small keys-only sorts are replayed as a CUDA graph once the same buffers come back: every
+    replay recomputes the plan from the new data (uniform, skewed, narrow, all-equal inputs
+    alternate through the same buffers) and equals np.sort."""
+    rng = np.random.default_rng(n)
+    w = torch.empty(n, dtype=torch.int64, device=dev)
+    s = torch.empty_like(w)
+    kinds = ["uniform", "low40", "uniform", "dups", "cluster", "uniform", "equal", "uniform"]
+    for i, kind in enumerate(kinds):
+        x = ak.bench_keys(42, i, n, np.int64) if kind == "uniform" else (
+            np.full(n, 7, dtype=np.int64) if kind == "equal" else dist(rng, n, kind))
+        w.copy_(torch.from_numpy(x))
+        ak.merge_sort(w, s, ex)
+        assert np.array_equal(w.cpu().numpy(), np.sort(x)), f"call {i} ({kind})"
