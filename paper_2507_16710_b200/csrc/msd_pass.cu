@@ -203,8 +203,17 @@ struct mp_smem {
     static constexpr std::size_t total = misc_off + 16;
 };
 
-// LEVEL 0: one 8-bit digit chosen on the device (plan = {mode, shift}: mode != 0 -> no-op),
-// cursors = that digit's exclusive offsets (small keys-only sorts, no host round trip).
+// Digit geometry of a partition level: the keys are already ordered by their top PB bits
+// (PB = 0: first level) and are partitioned by the next DB bits; cursor index = the top
+// PB + DB bits. LEVEL 1/2/3: 8-bit digits (8-, 16- and 24-bit buckets); LEVEL 0: one 8-bit
+// digit chosen on the device (plan = {mode, shift}: mode != 0 -> no-op; small sorts).
+template <int LEVEL>
+struct mp_level {
+    static constexpr int PB = LEVEL == 2 ? 8 : LEVEL == 3 ? 16 : 0;
+    static constexpr int DB = 8;
+    static constexpr int TOP = 64 - PB - DB;
+};
+
 template <typename T, int LEVEL>
 __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     msd_pass_kernel(const T* __restrict__ in, T* __restrict__ out, std::uint64_t n, int desc,
@@ -227,17 +236,19 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     if constexpr (LEVEL == 0) {
         if (plan[0] != 0) return;
     }
-    const int TOP = LEVEL == 0 ? plan[1] : 64 - 8 * LEVEL;  // shift of the 8L-bit prefix (digit)
+    using G = mp_level<LEVEL>;
+    constexpr int DB = G::DB;
+    const int TOP = LEVEL == 0 ? plan[1] : G::TOP;  // shift of the digit (cursor index = key >> TOP)
     constexpr std::uint32_t DMASK = LEVEL == 0 ? 0xffu : 0xffffffffu;
     std::uint32_t lo16 = 0, span = 1;
-    if (LEVEL >= 2) {
-        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> (TOP + 8));
-        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> (TOP + 8));
-        lo16 = f << 8;
+    if constexpr (G::PB > 0) {
+        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> (TOP + DB));
+        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> (TOP + DB));
+        lo16 = f << DB;
         span = l - f + 1;
     }
-    const std::uint32_t nbins = LEVEL <= 1 ? 256u : 256u * span;
-    if (LEVEL >= 2 && span > MP_SPAN) {
+    const std::uint32_t nbins = span << DB;
+    if (G::PB > 0 && span > MP_SPAN) {
         // tiny buckets (skewed keys): per-key cursor claims, written straight out
         for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
             const T k = in[t0 + j];
@@ -287,8 +298,9 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     // bin starts: thread t owns whole bins [t*BPT, t*BPT + BPT) (BPT <= 2) and their PARTS
     // sub-counters; exclusive scan in (bin, part) order + one global claim per non-empty bin
     {
-        constexpr int MAXC = 2 * MP_PARTS;
-        const std::uint32_t bpt = nbins > MP_BLOCK ? 2u : 1u;
+        constexpr int BPTMAX = MP_BINS / MP_BLOCK;  // bins per thread (<= 4)
+        constexpr int MAXC = BPTMAX * MP_PARTS;
+        const std::uint32_t bpt = nbins > 2 * MP_BLOCK ? 4u : nbins > MP_BLOCK ? 2u : 1u;
         const std::uint32_t fs = static_cast<std::uint32_t>(tid) * bpt * MP_PARTS;  // first sub-counter
         const std::uint32_t nsub = nbins * MP_PARTS;
         std::uint32_t c[MAXC];
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
         // global position of staged slot j in bin b = gofs[b] + j
         std::uint32_t r2 = run;
 #pragma unroll
-        for (int bi = 0; bi < 2; ++bi) {
+        for (int bi = 0; bi < BPTMAX; ++bi) {
             const std::uint32_t bin = fs / MP_PARTS + bi;
             std::uint32_t tot = 0;
 #pragma unroll
@@ -347,42 +359,46 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     (void)s_misc;
 }
 
-// Third level: histogram of the 24-bit prefixes of a 16-bit-partitioned array. A tile spans
-// few 16-bit buckets (relative bins in shared memory), flushed with one global atomic per
-// non-empty bin into hist24[2^24] (u32 counts; n < 2^32 per sort).
-template <typename T>
-__global__ void __launch_bounds__(MP_BLOCK) hist24_kernel(const T* __restrict__ in, std::uint64_t n, int desc,
-                                                        std::uint32_t* __restrict__ hist24) {
-    __shared__ std::uint32_t s_cnt[MP_BINS];
+// Histogram of the prefixes one DB-bit digit below an existing partition: the array is ordered
+// by its top (64 - PS) bits; counts of the prefixes key >> (PS - DB). A tile spans few buckets
+// of the existing partition (relative bins in shared memory), flushed with one global atomic
+// per non-empty bin into hist[2^(64 - PS + DB)] (u32 counts; n < 2^32 per sort).
+// PS = 48, DB = 8: the 24-bit prefixes under 16-bit buckets; PS = 53, DB = 9: the 20-bit
+// prefixes under 11-bit buckets.
+template <typename T, int PS, int DB = 8>
+__global__ void __launch_bounds__(MP_BLOCK) hist_sub_kernel(const T* __restrict__ in, std::uint64_t n, int desc,
+                                                          std::uint32_t* __restrict__ hist) {
+    constexpr int SH = PS - DB;
+    __shared__ std::uint32_t s_cnt[(1 << DB) * MP_SPAN];
     const int tid = threadIdx.x;
     const bool dsc = desc != 0;
     const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * MP_TILE;
     const std::uint32_t len = static_cast<std::uint32_t>(n - t0 < MP_TILE ? n - t0 : MP_TILE);
-    const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> 48);
-    const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> 48);
-    const std::uint32_t lo = f << 8, span = l - f + 1;
+    const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> PS);
+    const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> PS);
+    const std::uint32_t lo = f << DB, span = l - f + 1;
     if (span > MP_SPAN) {
         for (std::uint32_t j = tid; j < len; j += MP_BLOCK)
-            atomicAdd(hist24 + static_cast<std::uint32_t>(ord64(in[t0 + j], dsc) >> 40), 1u);
+            atomicAdd(hist + static_cast<std::uint32_t>(ord64(in[t0 + j], dsc) >> SH), 1u);
         return;
     }
-    for (int i = tid; i < MP_BINS; i += MP_BLOCK) s_cnt[i] = 0;
+    for (int i = tid; i < (1 << DB) * MP_SPAN; i += MP_BLOCK) s_cnt[i] = 0;
     __syncthreads();
     if (len == MP_TILE && (reinterpret_cast<std::uintptr_t>(in + t0) & 15) == 0) {
         const uint4* v = reinterpret_cast<const uint4*>(in + t0);
 #pragma unroll 4
         for (int i = tid; i < MP_TILE / 2; i += MP_BLOCK) {
             const uint4 a = __ldg(v + i);
-            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(reinterpret_cast<const T*>(&a)[0], dsc) >> 40) - lo], 1u);
-            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(reinterpret_cast<const T*>(&a)[1], dsc) >> 40) - lo], 1u);
+            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(reinterpret_cast<const T*>(&a)[0], dsc) >> SH) - lo], 1u);
+            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(reinterpret_cast<const T*>(&a)[1], dsc) >> SH) - lo], 1u);
         }
     } else {
         for (std::uint32_t j = tid; j < len; j += MP_BLOCK)
-            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(in[t0 + j], dsc) >> 40) - lo], 1u);
+            atomicAdd(&s_cnt[static_cast<std::uint32_t>(ord64(in[t0 + j], dsc) >> SH) - lo], 1u);
     }
     __syncthreads();
-    for (std::uint32_t i = tid; i < 256 * span; i += MP_BLOCK)
-        if (s_cnt[i]) atomicAdd(hist24 + lo + i, s_cnt[i]);
+    for (std::uint32_t i = tid; i < (span << DB); i += MP_BLOCK)
+        if (s_cnt[i]) atomicAdd(hist + lo + i, s_cnt[i]);
 }
 
 // Exclusive scan of hist24 (2^24 u32) into cur24 (u64), three launches: chunk sums,
@@ -521,7 +537,7 @@ void msd_level3(ak_ctx* c, const T* kin, T* kout, std::uint64_t n, bool desc) {
     AKB_CUDA(cudaMemsetAsync(hist24, 0, (std::size_t(1) << 24) * sizeof(std::uint32_t), c->stream));
     const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
     int tok = ctx_prof_begin(c, KF_HIST);
-    hist24_kernel<T><<<tiles, MP_BLOCK, 0, c->stream>>>(kin, n, desc ? 1 : 0, hist24);
+    hist_sub_kernel<T, 48><<<tiles, MP_BLOCK, 0, c->stream>>>(kin, n, desc ? 1 : 0, hist24);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     constexpr int nchunks = (1 << 24) / S24_CHUNK;

@@ -148,3 +148,26 @@ def test_small_sort_graph_replays(ak, ex, dev, n):
         w.copy_(torch.from_numpy(x))
         ak.merge_sort(w, s, ex)
         assert np.array_equal(w.cpu().numpy(), np.sort(x)), f"call {i} ({kind})"
+
+
+@pytest.mark.parametrize("n,kind", [((1 << 29) + 12345, "uniform"), ((1 << 29) + 7, "dups"), (1 << 30, "uniform")])
+def test_hybrid_three_msd_levels(ak, ex, dev, n, kind):
+    """n >= 2^29: partitions by the top 8, 16 and 24 bits, then the counting stage. Checked by
+    sortedness + order-independent multiset fingerprint (a full host sort of 8 GiB is too slow)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(n)
+    if kind == "uniform":
+        x = torch.randint(-(1 << 62), 1 << 62, (n,), dtype=torch.int64, device=dev, generator=g) * 2 + 1
+    else:  # 2^20 distinct values spread over the whole range: heavy duplicates in every bucket
+        x = torch.randint(0, 1 << 20, (n,), dtype=torch.int64, device=dev, generator=g) * (1 << 43) - (1 << 62)
+    fp_in = _fp(x)
+    s = torch.empty_like(x)
+    ak.merge_sort(x, s, ex)
+    assert bool((x[1:] >= x[:-1]).all())
+    assert _fp(x) == fp_in
+
+
+def _fp(t):
+    z = t * -7046029254386353131
+    z = z ^ ((z >> 29) & ((1 << 35) - 1))
+    return int(t.numel()), int(z.sum()), int((z * (2 * t + 1)).sum())
