@@ -490,13 +490,18 @@ void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t
         hist_joint_kernel<T, false><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
+    msd_joint_scan(c, g_joint, g_hist);
+    c->kernel_launches += 1;
+}
+
+void msd_joint_scan(ak_ctx* c, std::uint64_t* g_joint, std::uint64_t* g_hist) {
     std::uint64_t* sums = g_joint + 2 * JOINT_BINS + 256 + 8;  // ctx_msd tail
     std::uint64_t* colpart = sums + JS_CTAS;
     joint_scan_a_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, sums, colpart, g_hist);
     joint_scan_b_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint + JOINT_BINS, g_joint + 2 * JOINT_BINS, sums, colpart,
                                                          g_hist);
     AKB_CUDA(cudaGetLastError());
-    c->kernel_launches += 1;
+    c->kernel_launches += 2;
 }
 
 template <typename T>

@@ -16,6 +16,11 @@ template <typename T>
 void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t* g_hist, std::uint64_t* g_joint,
               bool digit5);
 
+// Exclusive scan of a 65536-bin histogram g_joint[0 .. 65536) laid out as ctx_msd (16-bit
+// bucket starts at +65536, 8-bit bucket starts at +131072); g_hist rows 6 and 7 += the 8-bit
+// marginals (g_hist: 8 x 256 u64).
+void msd_joint_scan(ak_ctx* c, std::uint64_t* g_joint, std::uint64_t* g_hist);
+
 // Two partition passes (kin -> kmid by the top 8 bits, kmid -> kout by the top 16 bits);
 // afterwards kout is ordered by its top 16 bits (order inside a 16-bit bucket arbitrary).
 template <typename T>
