@@ -52,7 +52,8 @@ def parse():
     p.add_argument("--dtype", choices=["int64", "uint64"], default="int64")
     p.add_argument("--seed", type=int, default=42)
     p.add_argument("--transport", choices=["nccl", "ipc"], default="nccl",
-                   help="N>1 exchange: NCCL grouped send/recv, or the peer-store kernel over CUDA IPC mappings")
+                   help="N>1 exchange: NCCL grouped send/recv, or peer memory over CUDA IPC mappings "
+                        "(the merge reads the incoming runs straight from the peers)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-configs", action="store_true", help="skip the per-config table (N=1 only)")
@@ -602,7 +603,12 @@ def main():
     if world > 1 and fam["exchange"][1]:
         ex_ms = fam["exchange"][0] / fam["exchange"][1]
         sent = sent_per_step
-        line["nvlink"] = {"transport": args.transport, "exchange_ms_rank0": ex_ms,
+        line["nvlink"] = {"transport": args.transport,
+                          "exchange": ("NCCL grouped send/recv into receive buffers, then the P-way merge"
+                                       if args.transport == "nccl" else
+                                       "fused into the P-way merge: runs read straight from the peers' sorted "
+                                       "arrays through CUDA IPC mappings (exchange_ms = that merge)"),
+                          "exchange_ms_rank0": ex_ms,
                           "bytes_sent_per_gpu": sent, "bytes_sent_note": "max over ranks, counted by the communicator",
                           "bus_gbs": sent / 1e9 / (ex_ms / 1e3),
                           "peak_gbs": NVLINK_MEASURED_GBS, "peak_kind": "measured peer copy (B200_PROFILING.md)",

@@ -20,6 +20,9 @@
 //                 const std::vector<std::uint64_t>& recv_counts);
 //   std::uint64_t merge_runs(const std::vector<std::uint64_t>& bounds,
 //                            const std::vector<std::uint64_t>& recv_counts);  // sort 2 of 2
+//   const void* sorted_buffer() const;   // the sorted local keys (peers read their slices)
+//   std::uint64_t merge_from_peers(const std::vector<const void*>& peers,
+//                                  const std::vector<std::uint64_t>& count_matrix);
 #pragma once
 
 #include <algorithm>
@@ -89,6 +92,12 @@ struct comm_iface {
     virtual std::vector<char> recv_bytes(int /*src*/) {
         throw std::runtime_error("transport: point-to-point messages are not supported by this communicator");
     }
+    // Peer memory: every rank passes one device buffer; on success out[q] is rank q's buffer
+    // as addressable from this rank (the same process / GPU, or a CUDA IPC mapping over
+    // NVLink). Collective. false (nothing done) when the transport cannot map peers (NCCL).
+    virtual bool map_peers(const void* /*local*/, std::vector<const void*>& /*out*/) { return false; }
+    // after the ranks' reads of mapped peer buffers: every read has finished (collective)
+    virtual void peers_released() {}
     // rank_counters (sim_comm.hpp:33-39)
     struct counters_c {
         std::uint64_t p2p_sends = 0, p2p_bytes = 0, collective_ops = 0, collective_sends = 0,
@@ -408,7 +417,8 @@ refine_out refine_run(comm_iface& comm, Local& L, std::vector<T>& spl, std::uint
 // capacity is short. Collective.
 template <typename T, typename Local>
 void count_exchange(comm_iface& comm, Local& L, const std::vector<T>& spl, std::uint64_t n, std::uint64_t capacity,
-                    std::vector<std::uint64_t>& bounds, std::vector<std::uint64_t>& recv_counts) {
+                    std::vector<std::uint64_t>& bounds, std::vector<std::uint64_t>& recv_counts,
+                    std::vector<std::uint64_t>* matrix = nullptr) {
     const std::size_t P = static_cast<std::size_t>(comm.size());
     const std::size_t me = static_cast<std::size_t>(comm.rank());
     bounds.assign(P + 1, 0);
@@ -425,6 +435,7 @@ void count_exchange(comm_iface& comm, Local& L, const std::vector<T>& spl, std::
     comm.allgather(row.data(), row.size() * sizeof(std::uint64_t), mat.data());
     recv_counts.assign(P, 0);
     for (std::size_t s = 0; s < P; ++s) recv_counts[s] = mat[s * (P + 1) + me];
+    if (matrix) *matrix = mat;
     for (std::size_t r = 0; r < P; ++r) {
         std::uint64_t need = 0;
         for (std::size_t s = 0; s < P; ++s) need += mat[s * (P + 1) + r];
@@ -503,8 +514,8 @@ void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_
     }
 
     // redistribute (sihsort.hpp:472-501): slice_bounds + count exchange + payload
-    std::vector<std::uint64_t> bounds, recv_counts;
-    count_exchange<T>(comm, L, spl, n, L.capacity(), bounds, recv_counts);
+    std::vector<std::uint64_t> bounds, recv_counts, mat;
+    count_exchange<T>(comm, L, spl, n, L.capacity(), bounds, recv_counts, &mat);
     // (the count allgather replaces the reference's piggybacked counts: not a collective of the
     //  reference's accounting, so not counted in collective_ops)
     std::vector<std::uint64_t> row(P);
@@ -516,8 +527,17 @@ void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_
         st.redistribution_sends += 1;
         st.redistribution_bytes += tail ? (len + 1) * sizeof(T) : 8 + len * sizeof(T);
     }
-    L.exchange(comm, bounds, recv_counts);
-    st.output_count = L.merge_runs(bounds, recv_counts);  // local sort 2 of 2
+    // exchange + local sort 2 of 2: when the transport maps the peers' sorted arrays, the P-way
+    // merge reads every incoming run straight from its source rank (the all-to-all fused into
+    // the merge: no copy through a receive buffer); otherwise the runs are exchanged first
+    std::vector<const void*> peers;
+    if (P > 1 && comm.map_peers(L.sorted_buffer(), peers)) {
+        st.output_count = L.merge_from_peers(peers, mat);
+        comm.peers_released();
+    } else {
+        L.exchange(comm, bounds, recv_counts);
+        st.output_count = L.merge_runs(bounds, recv_counts);
+    }
     st.collective_ops = collectives;
     for (std::uint64_t i = 0; i < collectives; ++i) comm.count_collective();
     comm.ctr.p2p_sends += st.redistribution_sends;

@@ -270,6 +270,16 @@ comm_iface::counters_c loopback_comm::counters() const {
     return c;
 }
 
+bool loopback_comm::map_peers(const void* local, std::vector<const void*>& out) {
+    // every rank is a thread of this process on this GPU: its pointer is valid here as is
+    const std::uint64_t mine = reinterpret_cast<std::uint64_t>(local);
+    std::vector<std::uint64_t> all(w->P);
+    allgather(&mine, sizeof(mine), all.data());
+    out.resize(w->P);
+    for (int q = 0; q < w->P; ++q) out[q] = reinterpret_cast<const void*>(all[q]);
+    return true;
+}
+
 void loopback_world::abort() noexcept {
     {
         std::lock_guard<std::mutex> lk(mu);
@@ -354,6 +364,54 @@ char* allocation_base(const void* p) {
 ipc_comm::~ipc_comm() {
     for (auto& m : peers)
         if (m.base) cudaIpcCloseMemHandle(m.base);
+    for (auto& m : pulled)
+        if (m.base) cudaIpcCloseMemHandle(m.base);
+}
+
+char* ipc_comm::open_peer(mapping& m, const cudaIpcMemHandle_t& h) {
+    const char* hb = reinterpret_cast<const char*>(&h);
+    if (!m.base || m.handle.size() != sizeof(h) || std::memcmp(m.handle.data(), hb, sizeof(h)) != 0) {
+        if (m.base) AKB_CUDA(cudaIpcCloseMemHandle(m.base));
+        m.base = nullptr;
+        void* ptr = nullptr;
+        AKB_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        m.base = static_cast<char*>(ptr);
+        m.handle.assign(hb, hb + sizeof(h));
+    }
+    return m.base;
+}
+
+bool ipc_comm::map_peers(const void* local, std::vector<const void*>& out) {
+    struct rec {
+        cudaIpcMemHandle_t h;
+        std::uint64_t off;
+        std::uint64_t has;
+    };
+    rec mine{};
+    if (local) {
+        char* base = allocation_base(local);
+        AKB_CUDA(cudaIpcGetMemHandle(&mine.h, base));
+        mine.off = static_cast<std::uint64_t>(static_cast<const char*>(local) - base);
+        mine.has = 1;
+    }
+    std::vector<rec> all(p);
+    allgather(&mine, sizeof(rec), all.data());
+    out.assign(p, nullptr);
+    for (int q = 0; q < p; ++q) {
+        if (q == r) {
+            out[q] = local;
+            continue;
+        }
+        if (!all[q].has) continue;
+        out[q] = open_peer(pulled[q], all[q].h) + all[q].off;
+    }
+    return true;
+}
+
+void ipc_comm::peers_released() {
+    std::uint8_t one = 1;
+    std::vector<std::uint8_t> ack(p);
+    allgather(&one, 1, ack.data());
 }
 
 void ipc_comm::allgather(const void* in, std::size_t bytes, void* out) {
@@ -521,6 +579,41 @@ struct device_local {
         ctx_prof_end(c, tok);
     }
 
+    const void* sorted_buffer() const { return sorted; }
+
+    // The exchange fused into the P-way merge: run s is read straight from source rank s's
+    // sorted array (peers[s]: this GPU, or its HBM over NVLink through a CUDA IPC mapping),
+    // at the offset of this rank's slice there (row s of the count matrix), and merged in
+    // source-rank order into d_out -- no receive buffer, no separate copy pass.
+    std::uint64_t merge_from_peers(const std::vector<const void*>& peers, const std::vector<std::uint64_t>& mat) {
+        std::vector<const T*> ptrs;
+        std::vector<std::uint64_t> lens;
+        std::uint64_t total = 0, remote = 0;
+        for (std::size_t s = 0; s < P; ++s) {
+            const std::uint64_t len = mat[s * (P + 1) + me];
+            if (!len) continue;
+            std::uint64_t off = 0;
+            for (std::size_t d = 0; d < me; ++d) off += mat[s * (P + 1) + d];
+            if (!peers[s]) throw protocol_error("sihsort: a source rank with data mapped no buffer");
+            ptrs.push_back(static_cast<const T*>(peers[s]) + off);
+            lens.push_back(len);
+            total += len;
+            if (s != me) remote += len * sizeof(T);
+        }
+        if (total > cap) throw invalid_argument("sihsort: internal capacity");
+        const int tok = ctx_prof_begin(c, KF_EXCHANGE);  // transfer and merge are one step here
+        if (ptrs.size() == 1) {
+            AKB_CUDA(cudaMemcpyAsync(d_out, ptrs[0], total * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+        } else if (!ptrs.empty()) {
+            akb::merge_runs<T>(c, static_cast<int>(ptrs.size()), ptrs.data(), lens.data(), d_out, X, false);
+        }
+        ctx_prof_end(c, tok);
+        AKB_CUDA(cudaStreamSynchronize(c->stream));  // every read of peer memory has finished
+        pulled_bytes += remote;
+        return total;
+    }
+    std::uint64_t pulled_bytes = 0;
+
     // P-way merge of the runs in source-rank order (replaces local sort #2,
     // sihsort.hpp:555): merge_runs (K8), last level lands in d_out.
     std::uint64_t merge_runs(const std::vector<std::uint64_t>& bounds,
@@ -572,6 +665,8 @@ std::uint64_t sihsort_device(ak_ctx* c, comm_iface& comm, const T* d_in, std::ui
     device_local<T> L{c, d_in, n, d_out, cap, static_cast<std::size_t>(comm.size()),
                       static_cast<std::size_t>(comm.rank())};
     sihsort_run<T>(comm, L, cfg, st, splitters);
+    if (L.pulled_bytes)
+        if (auto* ic = dynamic_cast<ipc_comm*>(&comm)) ic->add_pulled(L.pulled_bytes);
     return st.output_count;
 }
 

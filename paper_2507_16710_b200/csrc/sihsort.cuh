@@ -71,7 +71,7 @@ struct ipc_comm final : comm_iface {
     };
     std::vector<mapping> peers;    // current mapping per peer rank
     ipc_comm(int rank_, int size_, int dev, void* u, akb_allgather_fn a, akb_allreduce_fn b)
-        : r(rank_), p(size_), device(dev), user(u), ag(a), ar(b), peers(size_) {}
+        : r(rank_), p(size_), device(dev), user(u), ag(a), ar(b), peers(size_), pulled(size_) {}
     ~ipc_comm() override;
     int rank() const override { return r; }
     int size() const override { return p; }
@@ -85,6 +85,12 @@ struct ipc_comm final : comm_iface {
         sm_count = sms;
     }
     std::uint64_t payload_bytes_sent() const override { return bytes_sent; }
+    bool map_peers(const void* local, std::vector<const void*>& out) override;
+    void peers_released() override;
+    void add_pulled(std::uint64_t b) { bytes_sent += b; }
+    // mappings of peer buffers for map_peers (separate from the receive-buffer ones)
+    std::vector<mapping> pulled;
+    char* open_peer(mapping& m, const cudaIpcMemHandle_t& h);
 };
 
 // P logical ranks in one process on one GPU (device analogue of sim::world,
@@ -131,6 +137,8 @@ struct loopback_comm final : comm_iface {
     void send_bytes(int dest, const void* p, std::size_t n, bool control) override;
     std::vector<char> recv_bytes(int src) override;
     counters_c counters() const override;
+    bool map_peers(const void* local, std::vector<const void*>& out) override;  // same process and GPU
+    void peers_released() override { w->barrier(); }
     int sm_count = 148;
 };
 

@@ -71,6 +71,20 @@ struct host_local {
         std::copy(all.begin(), all.end(), out);
         return all.size();
     }
+    // peer-mapped variant (only with a transport that maps peers; the callback one does not)
+    const void* sorted_buffer() const { return sorted.data(); }
+    std::uint64_t merge_from_peers(const std::vector<const void*>& peers, const std::vector<std::uint64_t>& mat) {
+        std::vector<T> all;
+        for (std::size_t s = 0; s < P; ++s) {
+            std::uint64_t off = 0;
+            for (std::size_t d = 0; d < me; ++d) off += mat[s * (P + 1) + d];
+            const T* src = static_cast<const T*>(peers[s]) + off;
+            all.insert(all.end(), src, src + mat[s * (P + 1) + me]);
+        }
+        std::stable_sort(all.begin(), all.end());
+        std::copy(all.begin(), all.end(), out);
+        return all.size();
+    }
 };
 
 thread_local std::string g_err;
