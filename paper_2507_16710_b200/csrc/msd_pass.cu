@@ -322,19 +322,25 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
 #pragma unroll
         for (int w = 0; w < MP_BLOCK / 32; ++w) wp += w < warp ? s_wsum[w] : 0u;
         std::uint32_t run = wp + inc - sum;
-        // global position of staged slot j in bin b = gofs[b] + j
+        // global position of staged slot j in bin b = gofs[b] + j. The cursor claims are issued
+        // here and their results consumed only after the keys are staged: the global atomic
+        // round trip overlaps the rewrite of the starts and the staging stores
         std::uint32_t r2 = run;
+        std::uint64_t gclaim[BPTMAX];
+        std::uint32_t gbase[BPTMAX];
 #pragma unroll
         for (int bi = 0; bi < BPTMAX; ++bi) {
             const std::uint32_t bin = fs / MP_PARTS + bi;
             std::uint32_t tot = 0;
 #pragma unroll
             for (int q = 0; q < MP_PARTS; ++q) tot += c[bi * MP_PARTS + q];
-            if (static_cast<std::uint32_t>(bi) < bpt && bin < nbins && tot) {
-                const std::uint64_t g = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + bin),
-                                                  static_cast<unsigned long long>(tot));
-                s_gofs[bin] = g - r2;
-            }
+            gclaim[bi] = 0;
+            gbase[bi] = r2;
+            if (static_cast<std::uint32_t>(bi) < bpt && bin < nbins && tot)
+                gclaim[bi] = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + bin),
+                                       static_cast<unsigned long long>(tot));
+            else
+                gbase[bi] = 0xffffffffu;  // no claim for this bin
             r2 += tot;
         }
         __syncthreads();  // every count read before the starts overwrite them
@@ -344,11 +350,14 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
                 s_cnt[fs + q] = run;
                 run += c[q];
             }
-    }
-    __syncthreads();
+        __syncthreads();
 #pragma unroll
-    for (int i = 0; i < MP_ITEMS; ++i)
-        if (item_ok(i)) s_stage[s_cnt[bin_of(k[i]) * MP_PARTS + part] + ((sl[i / 2] >> (16 * (i & 1))) & 0xffffu)] = k[i];
+        for (int i = 0; i < MP_ITEMS; ++i)
+            if (item_ok(i)) s_stage[s_cnt[bin_of(k[i]) * MP_PARTS + part] + ((sl[i / 2] >> (16 * (i & 1))) & 0xffffu)] = k[i];
+#pragma unroll
+        for (int bi = 0; bi < BPTMAX; ++bi)
+            if (gbase[bi] != 0xffffffffu) s_gofs[fs / MP_PARTS + bi] = gclaim[bi] - gbase[bi];
+    }
     __syncthreads();
     // contiguous per-bin runs: consecutive staged slots of one bin go to consecutive addresses
 #pragma unroll 4
