@@ -1582,7 +1582,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
         __syncthreads();
         // ---- each position ranks its key inside its bin: final slot = bin start + #(key, pos) smaller ----
         T* o = out + b;
-#pragma unroll 1
+#pragma unroll 3
         for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
             const B v = sb[x];
             const std::uint32_t bn = static_cast<std::uint32_t>(v >> shift) & bmask;
