@@ -5,7 +5,9 @@
 //     one host thread per rank (the reference's in-process world, sim_comm.hpp:41-218).
 //     Collectives are host-level; sihsort slices move device to device.
 //   * ak::nccl::rank_comm: one rank per GPU (one process or thread each) over NCCL,
-//     NVLink 5 / NVSwitch -- the production transport for the 8xB200 sample sort.
+//     NVLink 5 / NVSwitch -- the production transport for the 8xB200 sample sort;
+//   * ak::ipc::rank_comm: one process per GPU, peer memory through CUDA IPC (the exchange is
+//     fused into the merge), control collectives from caller callbacks.
 // Both abort on failure so blocked peers wake with sim::transport_error.
 #pragma once
 
@@ -228,5 +230,33 @@ private:
 };
 
 }  // namespace nccl
+
+namespace ipc {
+
+/// One process per GPU without NCCL: the SIHSort exchange reads the peers' sorted arrays
+/// through CUDA IPC mappings (fused into the P-way merge; NVLink P2P between GPUs, or
+/// processes sharing one GPU), and the caller supplies the tiny control collectives -- e.g.
+/// an MPI / gloo allgather of `bytes` per rank (rank order) and a u64 sum allreduce.
+class rank_comm : public detail::comm_ops<rank_comm> {
+public:
+    using allgather_fn = ak_allgather_fn;       // int (void* user, const void* in, uint64_t bytes, void* out)
+    using allreduce_fn = ak_allreduce_u64_fn;  // int (void* user, uint64_t* inout, uint64_t n)
+    rank_comm(std::size_t nranks, std::size_t rank, int device, void* user, allgather_fn ag, allreduce_fn ar) {
+        detail::check(ak_comm_ipc_create(static_cast<int>(nranks), static_cast<int>(rank), device, user, ag, ar, &c_));
+    }
+    rank_comm(const rank_comm&) = delete;
+    rank_comm& operator=(const rank_comm&) = delete;
+    ~rank_comm() {
+        if (c_) ak_comm_destroy(c_);
+    }
+    std::size_t rank() const noexcept { return static_cast<std::size_t>(ak_comm_rank(c_)); }
+    std::size_t world_size() const noexcept { return static_cast<std::size_t>(ak_comm_size(c_)); }
+    ak_comm* handle() const noexcept { return c_; }
+
+private:
+    ak_comm* c_ = nullptr;
+};
+
+}  // namespace ipc
 
 }  // namespace ak

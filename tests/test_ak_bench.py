@@ -82,3 +82,22 @@ def test_sort_weak_strong_csv(tmp_path, extra):
     r = run("sort-strong", "--dtype", "f32", "--n", 1_000_003, "--ranks", 1, "--reps", 3, *extra)
     assert r.returncode == 0, r.stderr
     assert "sort-strong" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_sort_weak_nccl_multi_gpu(orc, ranks):
+    """ak_bench with one rank per GPU over NCCL (thread per GPU, one process): per-rank output
+    counts and message counts equal the oracle's (skipped below `ranks` GPUs)."""
+    import torch
+    if torch.cuda.device_count() < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    n = 1 << 20
+    r = run("sihsort-sim", "--dtype", "i64", "--ranks", ranks, "--per-rank", n, "--reps", 3, "--transport", "nccl")
+    assert r.returncode == 0, r.stderr
+    st = stats_of(r.stdout)
+    import paper_2507_16710_b200 as ak
+    want, wstats, _ = orc.sihsort([ak.bench_keys(42, q, n, np.int64) for q in range(ranks)])
+    for q in range(ranks):
+        assert int(st[f"out_count_rank_{q}"]) == want[q].size
+        assert int(st[f"msg_count_rank_{q}"]) == wstats[q]["redistribution_sends"]
