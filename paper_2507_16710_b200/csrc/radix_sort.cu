@@ -1382,6 +1382,103 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
 // Measured and dropped (r02): settling only the keys that share a bin (random in-bin reads +
 // an in-place rewrite) 2.10 ms, and coarse 16-key bins ranked by warp shuffles 5.2 ms, vs
 // 1.78 ms for the per-position rank below (at 2^28 int64).
+// ---- helpers of the counting local stages (one CTA of LC_BLOCK threads; call from all threads) ----
+
+// Exclusive scan of nwords packed u16 bin counts (two per word) into packed u16 bin starts;
+// s_c16[2 * nwords] = len afterwards (the end of the last bin). Contains __syncthreads().
+__device__ __forceinline__ void lc_scan_counts(std::uint32_t* s_cw, std::uint32_t nwords, std::uint32_t len,
+                                               std::uint32_t* s_wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const std::uint32_t wpw = nwords / LC_WARPS;
+    const std::uint32_t nq = wpw / 128;
+    std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
+    if (nq >= 1) {
+        uint4 u[2];
+        std::uint32_t cs[2] = {0, 0};
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (q < static_cast<int>(nq)) {
+                u[q] = *reinterpret_cast<const uint4*>(wbase + q * 128);
+                const std::uint32_t S = u[q].x + u[q].y + u[q].z + u[q].w;
+                cs[q] = (S & 0xffffu) + (S >> 16);
+            }
+        std::uint32_t p = cs[0] | (cs[1] << 16);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(FULL, p, o);
+            if (lane >= o) p += y;
+        }
+        const std::uint32_t t = __shfl_sync(FULL, p, 31);
+        const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
+        if (lane == 0) s_wsum[warp] = T0 + T1;
+        __syncthreads();
+        std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
+        const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (q < static_cast<int>(nq)) {
+                std::uint32_t run = exq[q];
+                std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u[q]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
+                    wv[j] = run | ((run + lo) << 16);
+                    run += lo + hi;
+                }
+                *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
+            }
+    } else {
+        const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
+        const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
+        const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
+        const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
+        const std::uint32_t S = c0 + c1;
+        const std::uint32_t sum = (S & 0xffffu) + (S >> 16);
+        std::uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_wsum[warp] = inc;
+        __syncthreads();
+        std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
+        std::uint32_t run = wp + inc - sum;
+        if (w0 < nwords) {
+            const std::uint32_t lo = c0 & 0xffffu, hi = c0 >> 16;
+            s_cw[w0] = run | ((run + lo) << 16);
+            run += lo + hi;
+        }
+        if (wpt == 2 && w0 + 1 < nwords) s_cw[w0 + 1] = run | ((run + (c1 & 0xffffu)) << 16);
+    }
+    if (tid == 0) reinterpret_cast<std::uint16_t*>(s_cw)[2 * nwords] = static_cast<std::uint16_t>(len);
+}
+
+// Each staged position x ranks its key inside its bin (bins = ((v - kmin) >> shift) & bmask,
+// starts in s_c16, staged keys in sb, bin order): final slot = bin start + #(key, position)
+// lexicographically smaller; store(rank, key) is called once per position.
+template <typename B, typename Store>
+__device__ __forceinline__ void lc_rank_store(const B* sb, const std::uint16_t* s_c16, std::uint32_t len, B kmin,
+                                              int shift, std::uint32_t bmask, Store&& store) {
+#pragma unroll 3
+    for (std::uint32_t x = threadIdx.x; x < len; x += LC_BLOCK) {
+        const B v = sb[x];
+        const std::uint32_t bn = static_cast<std::uint32_t>((v - kmin) >> shift) & bmask;
+        const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
+        std::uint32_t rk = x;
+        if (cnt > 1) {
+            rk = st + lex_less96(sb[st], st, v, x) + lex_less96(sb[st + 1], st + 1, v, x);
+#pragma unroll 1
+            for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(sb[y], y, v, x);
+        }
+        store(rk, v);
+    }
+}
+
 template <typename T, int ITEMS, bool DESC>
 __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
     local_count3_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
@@ -1504,75 +1601,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
             continue;
         }
         // ---- exclusive scan of the packed counts -> packed u16 bin starts (as local_count) ----
-        {
-            const std::uint32_t wpw = nwords / LC_WARPS;
-            const std::uint32_t nq = wpw / 128;
-            std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
-            if (nq >= 1) {
-                uint4 u[2];
-                std::uint32_t cs[2] = {0, 0};
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    if (q < static_cast<int>(nq)) {
-                        u[q] = *reinterpret_cast<const uint4*>(wbase + q * 128);
-                        const std::uint32_t S = u[q].x + u[q].y + u[q].z + u[q].w;
-                        cs[q] = (S & 0xffffu) + (S >> 16);
-                    }
-                std::uint32_t p = cs[0] | (cs[1] << 16);
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const std::uint32_t y = __shfl_up_sync(FULL, p, o);
-                    if (lane >= o) p += y;
-                }
-                const std::uint32_t t = __shfl_sync(FULL, p, 31);
-                const std::uint32_t T0 = t & 0xffffu, T1 = t >> 16;
-                if (lane == 0) s_wsum[warp] = T0 + T1;
-                __syncthreads();
-                std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
-                const std::uint32_t exq[2] = {wp + (p & 0xffffu) - cs[0], wp + T0 + (p >> 16) - cs[1]};
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                    if (q < static_cast<int>(nq)) {
-                        std::uint32_t run = exq[q];
-                        std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u[q]);
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
-                            wv[j] = run | ((run + lo) << 16);
-                            run += lo + hi;
-                        }
-                        *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
-                    }
-            } else {
-                const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
-                const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
-                const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
-                const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
-                const std::uint32_t S = c0 + c1;
-                const std::uint32_t sum = (S & 0xffffu) + (S >> 16);
-                std::uint32_t inc = sum;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                if (lane == 31) s_wsum[warp] = inc;
-                __syncthreads();
-                std::uint32_t wp = lane < warp ? s_wsum[lane] : 0u;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) wp += __shfl_xor_sync(FULL, wp, o);
-                std::uint32_t run = wp + inc - sum;
-                if (w0 < nwords) {
-                    const std::uint32_t lo = c0 & 0xffffu, hi = c0 >> 16;
-                    s_cw[w0] = run | ((run + lo) << 16);
-                    run += lo + hi;
-                }
-                if (wpt == 2 && w0 + 1 < nwords) s_cw[w0 + 1] = run | ((run + (c1 & 0xffffu)) << 16);
-            }
-            if (tid == 0) reinterpret_cast<std::uint16_t*>(s_cw)[2 * nwords] = static_cast<std::uint16_t>(len);
-        }
+        lc_scan_counts(s_cw, nwords, len, s_wsum);
         __syncthreads();
         // ---- keys into bin order (the range's own TMA buffer is free: keys are in registers) ----
 #pragma unroll
@@ -1581,20 +1610,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
                 sb[s_c16[static_cast<std::uint32_t>(k[i] >> shift) & bmask] + ((sl[i / 5] >> (6 * (i % 5))) & 0x3fu)] = k[i];
         __syncthreads();
         // ---- each position ranks its key inside its bin: final slot = bin start + #(key, pos) smaller ----
-        T* o = out + b;
-#pragma unroll 3
-        for (std::uint32_t x = tid; x < len; x += LC_BLOCK) {
-            const B v = sb[x];
-            const std::uint32_t bn = static_cast<std::uint32_t>(v >> shift) & bmask;
-            const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
-            std::uint32_t rk = x;
-            if (cnt > 1) {
-                rk = st + lex_less96(sb[st], st, v, x) + lex_less96(sb[st + 1], st + 1, v, x);
-#pragma unroll 1
-                for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(sb[y], y, v, x);
-            }
-            o[rk] = static_cast<T>(v ^ X);
-        }
+        lc_rank_store<B>(sb, s_c16, len, B(0), shift, bmask, [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>(v ^ X); });
     }  // ranges
 }
 

@@ -171,3 +171,58 @@ def _fp(t):
     z = t * -7046029254386353131
     z = z ^ ((z >> 29) & ((1 << 35) - 1))
     return int(t.numel()), int(z.sum()), int((z * (2 * t + 1)).sum())
+
+
+def _top13(rng, n, low):
+    """Top 13 bits uniform (16-bit MSD buckets of ~n / 8192 keys, over one counting CTA from
+    n ~ 2^26 on: the plan takes three MSD levels well below 2^29), the low 51 bits from `low`."""
+    hi = rng.integers(0, 1 << 13, n, dtype=np.int64) << 51
+    return hi | low
+
+
+@pytest.mark.parametrize("kind", ["uniform", "dups", "const", "narrow", "oversized"])
+@pytest.mark.parametrize("desc", [False, True])
+def test_three_levels_narrow_top(ak, ex, dev, kind, desc):
+    """Three MSD levels at 2^26 (the digit-5 histogram re-read, msd_level3, 24-bit range cuts)
+    under skew: uniform, dups (bins over 48 keys: the redo kernel), const (every 24-bit
+    bucket one value), narrow (60 % of each bucket in a 2^30-wide sliver), oversized (one
+    top-13 value holds 40000 keys)."""
+    n = (1 << 26) + 2 * len(kind) + 1
+    rng = np.random.default_rng(len(kind) + 100 * desc)
+    if kind == "uniform":
+        x = _top13(rng, n, rng.integers(0, 1 << 51, n, dtype=np.int64))
+    elif kind == "dups":
+        x = _top13(rng, n, rng.integers(0, 3, n, dtype=np.int64) << 20)
+    elif kind == "const":
+        x = _top13(rng, n, np.int64(0))
+    elif kind == "narrow":  # 60 % of every bucket within 2^30 of its start
+        low = rng.integers(0, 1 << 51, n, dtype=np.int64)
+        sel = rng.random(n) < 0.6
+        low[sel] = rng.integers(0, 1 << 30, int(sel.sum()), dtype=np.int64)
+        x = _top13(rng, n, low)
+    else:  # one top-13 value holds 40000 keys
+        x = _top13(rng, n, rng.integers(0, 1 << 51, n, dtype=np.int64))
+        x[rng.integers(0, n, 40000)] = (np.int64(77) << 51) | rng.integers(0, 1 << 40, 40000, dtype=np.int64)
+    d = torch.from_numpy(x).to(dev)
+    ak.merge_sort(d, ex=ex, cmp="greater" if desc else None)
+    want = np.sort(x)
+    assert np.array_equal(d.cpu().numpy(), want[::-1] if desc else want)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "oversized"])
+def test_three_levels_uint64(ak, ex, dev, kind):
+    """~16K-key 16-bit buckets (n = 2^27, top 13 bits uniform), uint64 keys; oversized: one
+    bucket holds 30000 extra keys in an arithmetic run. Checked on the device."""
+    n = 1 << 27
+    g = torch.Generator(device=dev)
+    g.manual_seed(27 + len(kind))
+    x = (torch.randint(0, 1 << 13, (n,), dtype=torch.int64, device=dev, generator=g) << 51) | torch.randint(
+        0, 1 << 51, (n,), dtype=torch.int64, device=dev, generator=g)
+    if kind == "oversized":
+        x[:30000] = (5 << 51) + torch.arange(30000, device=dev) * 977
+    fp_in = _fp(x)
+    u = x.view(torch.uint64)
+    ak.merge_sort(u, ex=ex)
+    y = x ^ (-(1 << 63))  # uint64 order as int64 order
+    assert bool((y[1:] >= y[:-1]).all())
+    assert _fp(x) == fp_in
