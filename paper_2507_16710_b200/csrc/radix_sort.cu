@@ -1614,6 +1614,262 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
     }  // ranges
 }
 
+// Big-range counting stage (n >= 2^29 after two MSD levels): ranges of up to LB_CAP = 18432
+// keys -- a whole 16-bit bucket of a 2^30-key sort -- in ONE CTA per SM (the key buffer takes
+// 144 KB of shared memory; 36 keys per thread in registers), so two partition levels suffice
+// where the 4608-key stage needed a third level and its 24-bit histogram. The algorithm is
+// local_count3's (up to 2^15 packed u16 bins, one shared atomic per key, scan, bin-order
+// scatter, per-position rank); the differences: bins over the offset to the range's minimum
+// (min / max reduction: a range of several buckets may straddle an aligned boundary, where
+// OR-reduced varying bits would put nearly every key in a few bins), the single buffer (the
+// next range's TMA copy is issued once this range's rank loop is done) and the scan over up
+// to 16384 counter words. A bin over LC_MAX_BIN keys sends the range to the segment fallback
+// (big list: the stable redo kernel holds only 6144 keys).
+constexpr int LB_BLOCK = 512;
+constexpr int LB_ITEMS = 36;
+constexpr int LB_CAP = LB_BLOCK * LB_ITEMS;  // 18432 keys
+constexpr int LB_MAX_BITS = 15;
+constexpr int LB_WORDS = (1 << LB_MAX_BITS) / 2;  // 16384 counter words = 64 KB
+
+template <typename T>
+struct lb_smem {
+    static constexpr std::size_t buf_bytes = (sizeof(T) * (LB_CAP + 2) + 15) & ~std::size_t(15);
+    static constexpr std::size_t buf_off = 0;
+    static constexpr std::size_t cnt_off = buf_bytes;
+    static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LB_WORDS + 4);
+    static constexpr std::size_t red_off = cnt_off + cnt_bytes;                 // 2 x WARPS x u64 (min, max)
+    static constexpr std::size_t wsum_off = red_off + 2 * LC_WARPS * sizeof(std::uint64_t);
+    static constexpr std::size_t bar_off = wsum_off + LC_WARPS * sizeof(std::uint32_t);
+    static constexpr std::size_t total = bar_off + sizeof(std::uint64_t);
+};
+
+// Exclusive scan of nwords (a power of two, <= LB_WORDS) packed u16 counts into packed u16
+// starts: warp w owns words [w * wpw, (w + 1) * wpw); within it, row q of 128 words is read
+// as one 16-byte quad per lane (conflict-free). Contains __syncthreads().
+__device__ __forceinline__ void lb_scan_counts(std::uint32_t* s_cw, std::uint32_t nwords, std::uint32_t len,
+                                               std::uint32_t* s_wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const std::uint32_t wpw = nwords / LC_WARPS;
+    if (wpw < 128) {  // small tables: the single-CTA stage's scan
+        lc_scan_counts(s_cw, nwords, len, s_wsum);
+        return;
+    }
+    const std::uint32_t nq = wpw / 128;  // 1 .. 8
+    std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
+    // pass 1: the warp's total; pass 2: per row, a warp scan of the quad sums (recomputed
+    // rather than kept: registers hold the range's keys)
+    std::uint32_t tot = 0;
+#pragma unroll 4
+    for (std::uint32_t q = 0; q < nq; ++q) {
+        const uint4 u = *reinterpret_cast<const uint4*>(wbase + q * 128);
+        const std::uint32_t S = u.x + u.y + u.z + u.w;
+        tot += (S & 0xffffu) + (S >> 16);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    if (lane == 0) s_wsum[warp] = tot;
+    __syncthreads();
+    std::uint32_t run = lane < warp ? s_wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) run += __shfl_xor_sync(FULL, run, o);
+#pragma unroll 1
+    for (std::uint32_t q = 0; q < nq; ++q) {
+        uint4 u = *reinterpret_cast<const uint4*>(wbase + q * 128);
+        const std::uint32_t S = u.x + u.y + u.z + u.w;
+        const std::uint32_t c = (S & 0xffffu) + (S >> 16);
+        std::uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const std::uint32_t y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        std::uint32_t r = run + inc - c;
+        run += __shfl_sync(FULL, inc, 31);
+        std::uint32_t* wv = reinterpret_cast<std::uint32_t*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const std::uint32_t lo = wv[j] & 0xffffu, hi = wv[j] >> 16;
+            wv[j] = r | ((r + lo) << 16);
+            r += lo + hi;
+        }
+        *reinterpret_cast<uint4*>(wbase + q * 128) = u;
+    }
+    if (tid == 0) reinterpret_cast<std::uint16_t*>(s_cw)[2 * nwords] = static_cast<std::uint16_t>(len);
+}
+
+template <typename T, bool DESC, bool MINMAX>
+__global__ void __launch_bounds__(LB_BLOCK, 1)
+    local_big_kernel(const T* __restrict__ in, T* out, const std::uint64_t* __restrict__ cuts, std::uint64_t J,
+                     std::uint64_t* big) {
+    using L = lb_smem<T>;
+    using B = typename key_traits<T>::bits;
+    constexpr int ITEMS = LB_ITEMS;
+    static_assert(sizeof(T) == 8, "8-byte keys");
+    constexpr B X = (std::is_signed_v<T> ? (B(1) << 63) : B(0)) ^ (DESC ? ~B(0) : B(0));  // raw <-> ordered
+    extern __shared__ __align__(16) unsigned char smem[];
+    B* s_red = reinterpret_cast<B*>(smem + L::red_off);
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    std::uint64_t* s_bar = reinterpret_cast<std::uint64_t*>(smem + L::bar_off);
+    std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + L::cnt_off);
+    const std::uint16_t* s_c16 = reinterpret_cast<const std::uint16_t*>(s_cw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto fits = [&](std::uint64_t rb, std::uint64_t re) {
+        return re > rb && re - rb <= static_cast<std::uint64_t>(LB_CAP);
+    };
+    auto issue = [&](std::uint32_t r) {  // one thread; the buffer is idle
+        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
+        if (!fits(rb, re)) return;
+        const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
+        const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
+        mbar_arrive_expect_tx(s_bar, bytes);
+        bulk_g2s(smem + L::buf_off, in + a0, bytes, s_bar);
+    };
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    const std::uint32_t nr = static_cast<std::uint32_t>(J);
+    if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x);
+    std::uint32_t phase = 0;
+    const bool copy_equal = in != out;
+
+#pragma unroll 1
+    for (std::uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
+        const std::uint64_t b = cuts[r], e = cuts[r + 1];
+        const bool ok_range = fits(b, e);
+        const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
+        B* sb = reinterpret_cast<B*>(smem + L::buf_off) + static_cast<std::uint32_t>(b & 1);
+        B k[ITEMS];
+        B mn = ~B(0), mx = 0;
+        if (ok_range) {
+            mbar_wait(s_bar, phase);
+            phase ^= 1u;
+            const B k0 = sb[0];
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                if (static_cast<std::uint32_t>(i * LB_BLOCK) >= len) break;  // rows past len stay unused
+                const std::uint32_t li = static_cast<std::uint32_t>(i * LB_BLOCK + tid);
+                const B v = (li < len ? sb[li] : k0) ^ X;  // padding repeats key 0 (neutral)
+                k[i] = v;
+                if constexpr (MINMAX) {
+                    mn = v < mn ? v : mn;
+                    mx = v > mx ? v : mx;
+                } else {
+                    mx |= v ^ (k0 ^ X);  // OR of the bits that differ from key 0
+                }
+            }
+        }
+        if constexpr (MINMAX) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const B a = __shfl_xor_sync(FULL, mn, o), z = __shfl_xor_sync(FULL, mx, o);
+                mn = a < mn ? a : mn;
+                mx = z > mx ? z : mx;
+            }
+            if (lane == 0) {
+                s_red[warp] = mn;
+                s_red[LC_WARPS + warp] = mx;
+            }
+        } else {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx |= __shfl_xor_sync(FULL, mx, o);
+            if (lane == 0) s_red[warp] = mx;
+        }
+        const int nb_want = min(LB_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
+        const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
+        if (nwords_w >= 4) {
+            for (int i = tid; i < nwords_w / 4; i += LB_BLOCK) reinterpret_cast<uint4*>(s_cw)[i] = make_uint4(0, 0, 0, 0);
+        } else if (tid < nwords_w) {
+            s_cw[tid] = 0;
+        }
+        __syncthreads();
+        bool done = !ok_range;
+        if (!ok_range && e - b > static_cast<std::uint64_t>(LB_CAP) && tid == 0) {
+            const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+            big[1 + slot] = r;
+        }
+        B vary = 0, kmin = 0;
+        if (!done) {
+            // lanes 0-15 fold the minima, 16-31 the maxima: bins over the offset to the range's
+            // minimum (a range of several buckets may straddle an aligned boundary)
+            // (!MINMAX: OR of the differing bits -- ranges of one aligned bucket -- and kmin = 0)
+            if constexpr (MINMAX) {
+                B x = s_red[lane];
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) {
+                    const B y = __shfl_xor_sync(FULL, x, o);
+                    x = lane < 16 ? (y < x ? y : x) : (y > x ? y : x);
+                }
+                kmin = __shfl_sync(FULL, x, 0);
+                vary = __shfl_sync(FULL, x, 16) - kmin;
+            } else {
+                vary = lane < LC_WARPS ? s_red[lane] : B(0);
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
+                vary = __shfl_sync(FULL, vary, 0);
+            }
+            if (vary == 0) {  // every key equal
+                if (copy_equal)
+                    for (std::uint32_t j = tid; j < len; j += LB_BLOCK) out[b + j] = static_cast<T>(k[0] ^ X);
+                done = true;
+            }
+        }
+        if (!done) {
+            const int hb = 63 - __clzll(static_cast<long long>(vary));
+            const int nb = max(1, min(nb_want, hb + 1));
+            const int shift = hb + 1 - nb;
+            const std::uint32_t bmask = (1u << nb) - 1u;
+            const std::uint32_t nwords = 1u << (nb - 1);
+            constexpr int SW = (ITEMS + 4) / 5;
+            std::uint32_t sl[SW];
+#pragma unroll
+            for (int w = 0; w < SW; ++w) sl[w] = 0;
+            if constexpr (MINMAX) {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) k[i] -= kmin;  // offsets from here on (order kept)
+            }
+            bool over = false;
+            // item rows past len are skipped by block-uniform branches (ranges of several
+            // buckets are ~half full at 2^29)
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                if (static_cast<std::uint32_t>(i * LB_BLOCK) >= len) break;
+                const bool ok = static_cast<std::uint32_t>(i * LB_BLOCK + tid) < len;
+                const std::uint32_t bn = static_cast<std::uint32_t>(k[i] >> shift) & bmask;
+                const std::uint32_t sh = (bn & 1u) << 4;
+                const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
+                const std::uint32_t slot = (old >> sh) & 0xffffu;
+                over |= ok && slot >= LC_MAX_BIN;
+                sl[i / 5] |= (slot & 0x3fu) << (6 * (i % 5));
+            }
+            if (__syncthreads_or(over)) {  // clustered keys: the segment fallback sorts the range
+                if (tid == 0) {
+                    const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+                    big[1 + slot] = r;
+                }
+            } else {
+                lb_scan_counts(s_cw, nwords, len, s_wsum);
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i) {
+                    if (static_cast<std::uint32_t>(i * LB_BLOCK) >= len) break;
+                    if (static_cast<std::uint32_t>(i * LB_BLOCK + tid) < len)
+                        sb[s_c16[static_cast<std::uint32_t>(k[i] >> shift) & bmask] + ((sl[i / 5] >> (6 * (i % 5))) & 0x3fu)] =
+                            k[i];
+                }
+                __syncthreads();
+                lc_rank_store<B>(sb, s_c16, len, B(0), shift, bmask,
+                                 [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>((v + kmin) ^ X); });
+            }
+        }
+        // the buffer and the counters are idle once every thread is here: next range's copy
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0 && r + gridDim.x < nr) issue(r + gridDim.x);
+    }  // ranges
+}
+
 // Device plan of a small keys-only sort (no host round trip): among the top three digits
 // (histograms in g_hist), the highest one that is not constant partitions the keys into 256
 // buckets by one onesweep pass. Writes plan = {mode, shift} (mode 0 = go; 1 = its largest
@@ -1973,6 +2229,29 @@ void sort_oversized(ak_ctx* c, const T* G, T* kout, T* kalt, std::uint64_t n, bo
     }
 }
 
+// 1: two MSD levels + the big-range stage at n >= 2^29; 0: three MSD levels + the 4608-key
+// stage (experiment builds: make variant DEFS=-DAKB_CFG_BIG_LOCAL=0)
+#ifndef AKB_CFG_BIG_LOCAL
+#define AKB_CFG_BIG_LOCAL 1
+#endif
+
+// minmax: ranges of several buckets (bins over the offset to the minimum); otherwise every
+// range is one aligned bucket (OR-reduced varying bits, cheaper)
+template <typename T>
+void launch_local_big(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc,
+                      bool minmax, std::uint64_t* big) {
+    using LB = lb_smem<T>;
+    auto kern = minmax ? (desc ? local_big_kernel<T, true, true> : local_big_kernel<T, false, true>)
+                       : (desc ? local_big_kernel<T, true, false> : local_big_kernel<T, false, false>);
+    smem_attr(c, kern, LB::total);
+    const int tok = ctx_prof_begin(c, KF_LOCAL);
+    kern<<<static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count))), LB_BLOCK,
+           LB::total, c->stream>>>(G, kout, cuts, J, big);
+    AKB_CUDA(cudaGetLastError());
+    ctx_prof_end(c, tok);
+    c->kernel_launches += 1;
+}
+
 constexpr std::uint64_t SMALL_DEVICE_MAX = std::uint64_t(1) << 21;  // device-planned path up to here
 
 // Small keys-only 64-bit integer sorts with NO host round trip before the last kernel: the top
@@ -2078,7 +2357,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     std::uint64_t* g_offs = g_hist + PASSES * RADIX;
     std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
     int m = 0, top = PASSES, items = LOCAL_MAX_ITEMS;
-    bool bucket_mode = false;
+    bool bucket_mode = false, big_local = false;
     std::uint64_t step = n, J = 1, base_id = 0;
     const T* G = kin;  // buffer holding the bucket-ordered keys
     std::uint64_t* msdbuf = nullptr;
@@ -2159,6 +2438,15 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
             }
             est *= static_cast<double>(maxbin(top - m, nullptr)) / static_cast<double>(n);
             const double need = est + 6.0 * std::sqrt(est) + 64.0;
+            if (AKB_CFG_BIG_LOCAL && m == 2 && env < 0 && need > LOCAL_TILE && need + 256.0 <= LB_CAP && msd_ok &&
+                top == PASSES && n < (std::uint64_t(1) << 32) && ((reinterpret_cast<std::uintptr_t>(kin) & 15) == 0) &&
+                ((reinterpret_cast<std::uintptr_t>(kalt) & 15) == 0)) {
+                // 16-bit buckets over the 4608-key stage but within LB_CAP: two MSD levels + the
+                // big-range stage instead of a third level (see local_big_kernel)
+                big_local = true;
+                bucket_mode = est >= 0.55 * LB_CAP;
+                break;
+            }
             if (need > LOCAL_TILE) continue;
             if (env > 0 && env != m) continue;
             const int ib = need <= LOCAL_BLOCK * 8 ? 8 : (need <= LOCAL_BLOCK * 12 ? 12 : 16);
@@ -2176,6 +2464,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
             break;
         }
         if (m > 3 || m > top) return false;
+        if (big_local && !bucket_mode) step = LB_CAP / 2;  // provisional (re-cut from the exact largest bucket)
         J = bucket_mode ? (1ull << (8 * m)) : ceil_div(n, step);
         base_id = prefix << (8 * m);
         hist_scan_kernel<<<PASSES, RADIX, 0, c->stream>>>(g_hist, g_offs);
@@ -2196,7 +2485,23 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                 msd_level3<T>(c, kout, kalt, n, desc);
                 cur = kalt;
             }
-            if (!bucket_mode) {
+            if (big_local && !bucket_mode) {
+                const std::uint64_t maxb = msd_max_bucket(c, m);
+                if (maxb + 256 <= static_cast<std::uint64_t>(LB_CAP)) {
+                    step = LB_CAP - maxb;
+                    J = ceil_div(n, step);
+                } else {  // a bucket over the big-range stage (skewed keys): a third level instead
+                    big_local = false;
+                    msd_level3<T>(c, kout, kalt, n, desc);
+                    cur = kalt;
+                    m = 3;
+                    items = 12;
+                    const std::uint64_t cap = static_cast<std::uint64_t>(LOCAL_BLOCK) * items;
+                    const std::uint64_t maxb3 = msd_max_bucket(c, 3);
+                    step = maxb3 + 256 <= cap ? cap - maxb3 : 256;
+                    J = ceil_div(n, step);
+                }
+            } else if (!bucket_mode) {
                 // ranges of several buckets: size them from the exact largest bucket (the
                 // plan's estimate assumes independent digits, which skewed keys -- e.g. the
                 // exponent-heavy top bits of composite float keys -- violate)
@@ -2249,7 +2554,10 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
 #endif
     bool counted = false;
     if constexpr (std::is_integral_v<T> && sizeof(T) == 8) {  // the only keys that reach here (see above)
-        if (local_count_env() != 0) {
+        if (big_local) {
+            launch_local_big<T>(c, G, kout, cuts, J, desc, !bucket_mode, big);
+            counted = true;
+        } else if (local_count_env() != 0) {
             if (items == 8) launch_local_count<T, 8>(c, G, kout, cuts, J, n, desc, low, big, redo);
             else if (items == 12) launch_local_count<T, 12>(c, G, kout, cuts, J, n, desc, low, big, redo);
             else launch_local_count<T, 16>(c, G, kout, cuts, J, n, desc, low, big, redo);

@@ -151,9 +151,11 @@ def test_small_sort_graph_replays(ak, ex, dev, n):
 
 
 @pytest.mark.parametrize("n,kind", [((1 << 29) + 12345, "uniform"), ((1 << 29) + 7, "dups"), (1 << 30, "uniform")])
-def test_hybrid_three_msd_levels(ak, ex, dev, n, kind):
-    """n >= 2^29: partitions by the top 8, 16 and 24 bits, then the counting stage. Checked by
-    sortedness + order-independent multiset fingerprint (a full host sort of 8 GiB is too slow)."""
+def test_hybrid_big_range_stage(ak, ex, dev, n, kind):
+    """n >= 2^29: partitions by the top 8 and 16 bits, then the big-range counting stage
+    (local_big_kernel: whole 16-bit buckets of up to 18432 keys; range mode with min / max
+    bins at 2^29, one bucket per range at 2^30). Checked by sortedness + order-independent
+    multiset fingerprint (a full host sort of 8 GiB is too slow)."""
     g = torch.Generator(device=dev)
     g.manual_seed(n)
     if kind == "uniform":
@@ -174,19 +176,20 @@ def _fp(t):
 
 
 def _top13(rng, n, low):
-    """Top 13 bits uniform (16-bit MSD buckets of ~n / 8192 keys, over one counting CTA from
-    n ~ 2^26 on: the plan takes three MSD levels well below 2^29), the low 51 bits from `low`."""
+    """Top 13 bits uniform (16-bit MSD buckets of ~n / 8192 keys: over the 4608-key stage from
+    n ~ 2^26 on, so the big-range stage runs well below 2^29), the low 51 bits from `low`."""
     hi = rng.integers(0, 1 << 13, n, dtype=np.int64) << 51
     return hi | low
 
 
 @pytest.mark.parametrize("kind", ["uniform", "dups", "const", "narrow", "oversized"])
 @pytest.mark.parametrize("desc", [False, True])
-def test_three_levels_narrow_top(ak, ex, dev, kind, desc):
-    """Three MSD levels at 2^26 (the digit-5 histogram re-read, msd_level3, 24-bit range cuts)
-    under skew: uniform, dups (bins over 48 keys: the redo kernel), const (every 24-bit
-    bucket one value), narrow (60 % of each bucket in a 2^30-wide sliver), oversized (one
-    top-13 value holds 40000 keys)."""
+def test_big_range_stage_skew(ak, ex, dev, kind, desc):
+    """local_big_kernel at 2^26 in range mode (ranges of one or two ~8K-key buckets, bins over
+    the offset to the range minimum) under skew: uniform, dups (bins over 48 keys: the
+    segment fallback), const (every 16-bit bucket one value), narrow (60 % of each bucket in
+    a 2^30-wide sliver), oversized (one top-13 value holds 40000 keys: a bucket over 18432
+    keys, so the plan falls back to a third MSD level and the 4608-key stage)."""
     n = (1 << 26) + 2 * len(kind) + 1
     rng = np.random.default_rng(len(kind) + 100 * desc)
     if kind == "uniform":
@@ -210,9 +213,10 @@ def test_three_levels_narrow_top(ak, ex, dev, kind, desc):
 
 
 @pytest.mark.parametrize("kind", ["uniform", "oversized"])
-def test_three_levels_uint64(ak, ex, dev, kind):
-    """~16K-key 16-bit buckets (n = 2^27, top 13 bits uniform), uint64 keys; oversized: one
-    bucket holds 30000 extra keys in an arithmetic run. Checked on the device."""
+def test_big_range_stage_bucket_mode(ak, ex, dev, kind):
+    """~16K-key 16-bit buckets (n = 2^27, top 13 bits uniform): local_big_kernel with one
+    bucket per range (OR-reduced varying bits), uint64 keys; oversized: one bucket holds
+    30000 extra keys (over 18432: the segment fallback). Checked on the device."""
     n = 1 << 27
     g = torch.Generator(device=dev)
     g.manual_seed(27 + len(kind))
