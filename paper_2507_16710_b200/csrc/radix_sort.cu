@@ -1534,6 +1534,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
             const B k0 = sb[0];
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
+                if (static_cast<std::uint32_t>(i * LC_BLOCK) >= len) break;  // rows past len stay unused
                 const std::uint32_t li = static_cast<std::uint32_t>(i * LC_BLOCK + tid);
                 const B v = li < len ? sb[li] : k0;  // padding repeats key 0 (neutral below)
                 orx |= v ^ k0;
@@ -1585,6 +1586,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
         bool over = false;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
+            if (static_cast<std::uint32_t>(i * LC_BLOCK) >= len) break;
             const bool ok = static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len;
             const std::uint32_t bn = static_cast<std::uint32_t>(k[i] >> shift) & bmask;
             const std::uint32_t sh = (bn & 1u) << 4;
@@ -1605,9 +1607,11 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
         __syncthreads();
         // ---- keys into bin order (the range's own TMA buffer is free: keys are in registers) ----
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i)
+        for (int i = 0; i < ITEMS; ++i) {
+            if (static_cast<std::uint32_t>(i * LC_BLOCK) >= len) break;
             if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len)
                 sb[s_c16[static_cast<std::uint32_t>(k[i] >> shift) & bmask] + ((sl[i / 5] >> (6 * (i % 5))) & 0x3fu)] = k[i];
+        }
         __syncthreads();
         // ---- each position ranks its key inside its bin: final slot = bin start + #(key, pos) smaller ----
         lc_rank_store<B>(sb, s_c16, len, B(0), shift, bmask, [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>(v ^ X); });
