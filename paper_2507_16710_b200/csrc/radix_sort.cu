@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "radix_sort.cuh"
+#include "tma.cuh"
 #include "msd_pass.cuh"
 #include "search_merge.cuh"
 
@@ -137,36 +138,6 @@ __device__ __forceinline__ void red_or_shared(std::uint32_t* addr, std::uint32_t
 }
 
 // TMA bulk copies (cp.async.bulk, non-tensor) completing on an mbarrier.
-__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
-    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_init_fence() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
-    asm volatile(
-        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
-            smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // Peer-lane discovery for the warp ranking (AKB_MATCH selects at run time):
 enum match_kind : int { MATCH_BALLOT = 0, MATCH_HW = 1, MATCH_SMEM = 2, MATCH_HYBRID = 3, MATCH_HALF = 4 };
 
