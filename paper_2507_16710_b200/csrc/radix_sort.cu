@@ -1353,14 +1353,15 @@ __global__ void __launch_bounds__(LC_BLOCK, lc_smem<T, ITEMS>::MINB)
 // Measured and dropped (r02): settling only the keys that share a bin (random in-bin reads +
 // an in-place rewrite) 2.10 ms, and coarse 16-key bins ranked by warp shuffles 5.2 ms, vs
 // 1.78 ms for the per-position rank below (at 2^28 int64).
-// ---- helpers of the counting local stages (one CTA of LC_BLOCK threads; call from all threads) ----
+// ---- helpers of the counting local stages (one CTA of NT threads; call from all threads) ----
 
 // Exclusive scan of nwords packed u16 bin counts (two per word) into packed u16 bin starts;
 // s_c16[2 * nwords] = len afterwards (the end of the last bin). Contains __syncthreads().
+template <int NT = LC_BLOCK>
 __device__ __forceinline__ void lc_scan_counts(std::uint32_t* s_cw, std::uint32_t nwords, std::uint32_t len,
                                                std::uint32_t* s_wsum) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const std::uint32_t wpw = nwords / LC_WARPS;
+    const std::uint32_t wpw = nwords / (NT / 32);
     const std::uint32_t nq = wpw / 128;
     std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
     if (nq >= 1) {
@@ -1401,7 +1402,7 @@ __device__ __forceinline__ void lc_scan_counts(std::uint32_t* s_cw, std::uint32_
                 *reinterpret_cast<uint4*>(wbase + q * 128) = u[q];
             }
     } else {
-        const std::uint32_t wpt = nwords > LC_BLOCK ? 2u : 1u;
+        const std::uint32_t wpt = nwords > NT ? 2u : 1u;
         const std::uint32_t w0 = static_cast<std::uint32_t>(tid) * wpt;
         const std::uint32_t c0 = w0 < nwords ? s_cw[w0] : 0u;
         const std::uint32_t c1 = (wpt == 2 && w0 + 1 < nwords) ? s_cw[w0 + 1] : 0u;
@@ -1432,11 +1433,11 @@ __device__ __forceinline__ void lc_scan_counts(std::uint32_t* s_cw, std::uint32_
 // Each staged position x ranks its key inside its bin (bins = ((v - kmin) >> shift) & bmask,
 // starts in s_c16, staged keys in sb, bin order): final slot = bin start + #(key, position)
 // lexicographically smaller; store(rank, key) is called once per position.
-template <typename B, typename Store>
+template <typename B, int NT = LC_BLOCK, typename Store>
 __device__ __forceinline__ void lc_rank_store(const B* sb, const std::uint16_t* s_c16, std::uint32_t len, B kmin,
                                               int shift, std::uint32_t bmask, Store&& store) {
 #pragma unroll 3
-    for (std::uint32_t x = threadIdx.x; x < len; x += LC_BLOCK) {
+    for (std::uint32_t x = threadIdx.x; x < len; x += NT) {
         const B v = sb[x];
         const std::uint32_t bn = static_cast<std::uint32_t>((v - kmin) >> shift) & bmask;
         const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
@@ -1591,7 +1592,7 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
 
 // Big-range counting stage (n >= 2^29 after two MSD levels): ranges of up to LB_CAP = 18432
 // keys -- a whole 16-bit bucket of a 2^30-key sort -- in ONE CTA per SM (the key buffer takes
-// 144 KB of shared memory; 36 keys per thread in registers), so two partition levels suffice
+// 144 KB of shared memory; 18 keys per thread of 1024 in registers), so two partition levels suffice
 // where the 4608-key stage needed a third level and its 24-bit histogram. The algorithm is
 // local_count3's (up to 2^15 packed u16 bins, one shared atomic per key, scan, bin-order
 // scatter, per-position rank); the differences: bins over the offset to the range's minimum
@@ -1600,8 +1601,12 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
 // next range's TMA copy is issued once this range's rank loop is done) and the scan over up
 // to 16384 counter words. A bin over LC_MAX_BIN keys sends the range to the segment fallback
 // (big list: the stable redo kernel holds only 6144 keys).
-constexpr int LB_BLOCK = 512;
-constexpr int LB_ITEMS = 36;
+#ifndef AKB_LB_BLOCK
+#define AKB_LB_BLOCK 1024
+#endif
+constexpr int LB_BLOCK = AKB_LB_BLOCK;
+constexpr int LB_WARPS = LB_BLOCK / 32;
+constexpr int LB_ITEMS = 18432 / LB_BLOCK;
 constexpr int LB_CAP = LB_BLOCK * LB_ITEMS;  // 18432 keys
 constexpr int LB_MAX_BITS = 15;
 constexpr int LB_WORDS = (1 << LB_MAX_BITS) / 2;  // 16384 counter words = 64 KB
@@ -1613,8 +1618,8 @@ struct lb_smem {
     static constexpr std::size_t cnt_off = buf_bytes;
     static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LB_WORDS + 4);
     static constexpr std::size_t red_off = cnt_off + cnt_bytes;                 // 2 x WARPS x u64 (min, max)
-    static constexpr std::size_t wsum_off = red_off + 2 * LC_WARPS * sizeof(std::uint64_t);
-    static constexpr std::size_t bar_off = wsum_off + LC_WARPS * sizeof(std::uint32_t);
+    static constexpr std::size_t wsum_off = red_off + 2 * LB_WARPS * sizeof(std::uint64_t);
+    static constexpr std::size_t bar_off = wsum_off + LB_WARPS * sizeof(std::uint32_t);
     static constexpr std::size_t total = bar_off + sizeof(std::uint64_t);
 };
 
@@ -1624,9 +1629,9 @@ struct lb_smem {
 __device__ __forceinline__ void lb_scan_counts(std::uint32_t* s_cw, std::uint32_t nwords, std::uint32_t len,
                                                std::uint32_t* s_wsum) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const std::uint32_t wpw = nwords / LC_WARPS;
+    const std::uint32_t wpw = nwords / LB_WARPS;
     if (wpw < 128) {  // small tables: the single-CTA stage's scan
-        lc_scan_counts(s_cw, nwords, len, s_wsum);
+        lc_scan_counts<LB_BLOCK>(s_cw, nwords, len, s_wsum);
         return;
     }
     const std::uint32_t nq = wpw / 128;  // 1 .. 8
@@ -1744,7 +1749,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
             }
             if (lane == 0) {
                 s_red[warp] = mn;
-                s_red[LC_WARPS + warp] = mx;
+                s_red[LB_WARPS + warp] = mx;
             }
         } else {
 #pragma unroll
@@ -1770,19 +1775,19 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
             // minimum (a range of several buckets may straddle an aligned boundary)
             // (!MINMAX: OR of the differing bits -- ranges of one aligned bucket -- and kmin = 0)
             if constexpr (MINMAX) {
-                B x = s_red[lane];
+                B a = lane < LB_WARPS ? s_red[lane] : ~B(0), z = lane < LB_WARPS ? s_red[LB_WARPS + lane] : B(0);
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) {
-                    const B y = __shfl_xor_sync(FULL, x, o);
-                    x = lane < 16 ? (y < x ? y : x) : (y > x ? y : x);
+                for (int o = 16; o > 0; o >>= 1) {
+                    const B a2 = __shfl_xor_sync(FULL, a, o), z2 = __shfl_xor_sync(FULL, z, o);
+                    a = a2 < a ? a2 : a;
+                    z = z2 > z ? z2 : z;
                 }
-                kmin = __shfl_sync(FULL, x, 0);
-                vary = __shfl_sync(FULL, x, 16) - kmin;
+                kmin = a;
+                vary = z - a;
             } else {
-                vary = lane < LC_WARPS ? s_red[lane] : B(0);
+                vary = lane < LB_WARPS ? s_red[lane] : B(0);
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
-                vary = __shfl_sync(FULL, vary, 0);
+                for (int o = 16; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
             }
             if (vary == 0) {  // every key equal
                 if (copy_equal)
@@ -1834,7 +1839,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
                             k[i];
                 }
                 __syncthreads();
-                lc_rank_store<B>(sb, s_c16, len, B(0), shift, bmask,
+                lc_rank_store<B, LB_BLOCK>(sb, s_c16, len, B(0), shift, bmask,
                                  [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>((v + kmin) ^ X); });
             }
         }
