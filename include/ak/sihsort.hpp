@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <type_traits>
 #include <utility>
+#include <tuple>
 #include <vector>
 
 #include "ak/exec.hpp"
@@ -124,6 +125,11 @@ struct device_view {
     inline int c_sihsort(ak_ctx* c, ak_comm* cm, const T* in, std::uint64_t n, T* out, std::uint64_t cap,      \
                          std::uint64_t* cnt, const ak_sih_config* cfg, ak_sih_stats* st) {                    \
         return ak_sihsort_##S(c, cm, in, n, out, cap, cnt, cfg, st);                                          \
+    }                                                                                                         \
+    inline int c_sihsort_perm(ak_ctx* c, ak_comm* cm, const T* in, std::uint64_t n, T* out,                  \
+                              std::uint64_t* idx, std::uint64_t cap, std::uint64_t* cnt,                     \
+                              const ak_sih_config* cfg, ak_sih_stats* st) {                                  \
+        return ak_sihsort_perm_##S(c, cm, in, n, out, idx, cap, cnt, cfg, st);                                \
     }
 AK_SIH_DISPATCH(i32, std::int32_t)
 AK_SIH_DISPATCH(u32, std::uint32_t)
@@ -176,6 +182,39 @@ std::pair<std::vector<T>, sih_stats> sihsort(std::vector<T> local_data, Comm& co
         std::vector<T> out(count);
         dout.download(out.data(), count);
         return {std::move(out), detail::from_c(st)};
+    }
+}
+
+/// Distributed sortperm (an extension: the reference's sihsort is keys-only,
+/// sihsort.hpp:472-501). Rank r's key i has global index (sum of the lower ranks' sizes) + i;
+/// returns this rank's slice of the globally STABLE order as (keys, global indices): the
+/// ranks' results concatenated are the sorted keys and the global sortperm. Collective.
+template <typename T, typename Comm>
+std::tuple<std::vector<T>, std::vector<std::uint64_t>, sih_stats> sihsort_perm(std::span<const T> local_data,
+                                                                              Comm& comm, const sih_config& cfg,
+                                                                              const exec_backend& ex) {
+    detail::require_key<T>();
+    const ak_sih_config c = detail::to_c(cfg);
+    ak_sih_stats st{};
+    const std::uint64_t n = local_data.size();
+    detail::device_view<T> din(ex.ctx(), local_data);
+    std::uint64_t cap = n + n / 4 + 4096;
+    std::uint64_t count = 0;
+    for (;;) {
+        detail::device_buffer<T> dout(ex.ctx(), cap);
+        detail::device_buffer<std::uint64_t> didx(ex.ctx(), cap);
+        const int rc =
+            detail::c_sihsort_perm(ex.ctx(), comm.handle(), din.p, n, dout.p, didx.p, cap, &count, &c, &st);
+        if (rc == AK_ECAPACITY) {  // raised on every rank together: all retry with room
+            cap = (count > cap ? count : cap) + cap / 8 + 4096;
+            continue;
+        }
+        detail::check(rc, count);
+        std::vector<T> keys(count);
+        std::vector<std::uint64_t> idx(count);
+        dout.download(keys.data(), count);
+        didx.download(idx.data(), count);
+        return {std::move(keys), std::move(idx), detail::from_c(st)};
     }
 }
 

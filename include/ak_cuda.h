@@ -150,6 +150,17 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int key_bytes);
     int ak_sihsort_loopback_##S(int device, uint64_t P, const T* const* in, const uint64_t* n,  \
                                 T* const* out, const uint64_t* out_cap, uint64_t* out_count,    \
                                 const ak_sih_config* cfg, ak_sih_stats* stats);                 \
+    /* distributed sortperm (new: the reference sihsort is keys-only, sihsort.hpp:472-501): */ \
+    /* this rank's slice of the globally STABLE order of all ranks' keys -> out (keys) and */   \
+    /* out_idx (global indices: rank r's key i is sum of the lower ranks' n + i); capacity */   \
+    /* out_cap for both; stats as sihsort plus the index bytes in redistribution_bytes */       \
+    int ak_sihsort_perm_##S(ak_ctx* ctx, ak_comm* comm, const T* in, uint64_t n, T* out,        \
+                            uint64_t* out_idx, uint64_t out_cap, uint64_t* out_count,           \
+                            const ak_sih_config* cfg, ak_sih_stats* stats);                     \
+    int ak_sihsort_perm_loopback_##S(int device, uint64_t P, const T* const* in,               \
+                                     const uint64_t* n, T* const* out, uint64_t* const* out_idx, \
+                                     const uint64_t* out_cap, uint64_t* out_count,              \
+                                     const ak_sih_config* cfg, ak_sih_stats* stats);            \
     /* sihsort stages. sample_local (sihsort.hpp:264-282): k order statistics of the sorted */  \
     /* device keys -> host_out[min(k, n)] */                                                    \
     int ak_sample_local_##S(ak_ctx* ctx, const T* sorted, uint64_t n, uint64_t k, T* host_out,   \

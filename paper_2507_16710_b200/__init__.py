@@ -873,6 +873,67 @@ def sihsort_loopback(inputs: list[torch.Tensor], cfg: SihConfig | None = None, c
     return [outs[r][: oc[r]] for r in range(P)], [stats[r] for r in range(P)]
 
 
+def sihsort_perm(local_data: torch.Tensor, comm: NcclComm | None = None, cfg: SihConfig | None = None,
+                 ex: ExecBackend | None = None, capacity: int | None = None):
+    """Distributed sortperm (new: the reference sihsort is keys-only, sihsort.hpp:472-501):
+    SIHSort of (key, global index) pairs. Rank r's key i has global index sum of the lower
+    ranks' counts + i. Returns (this rank's keys, their global indices as int64, SihStats);
+    the ranks' outputs concatenated are the globally stable sort order and its permutation."""
+    _dev(local_data, "sihsort_perm")
+    e = _ex(ex, local_data)
+    n = local_data.numel()
+    s = _suffix(local_data)
+    fn = _fn(f"ak_sihsort_perm_{s}", [_P, _P, _P, _U64, _P, _P, _U64, C.POINTER(_U64), C.POINTER(SihConfig),
+                                       C.POINTER(SihStats)])
+    cfg = cfg or SihConfig()
+    cap = capacity if capacity is not None else 2 * n + 1024
+    for _ in range(2):
+        out = torch.empty(cap, dtype=local_data.dtype, device=local_data.device)
+        idx = torch.empty(cap, dtype=torch.int64, device=local_data.device)
+        oc = _U64(0)
+        st = SihStats()
+        rc = fn(e.handle, comm.handle if comm else None, _ptr(local_data), n, _ptr(out), _ptr(idx), cap,
+                C.byref(oc), C.byref(cfg), C.byref(st))
+        if rc == 6 and capacity is None:
+            cap = int(oc.value)
+            continue
+        _check(rc, int(oc.value))
+        return out[: oc.value], idx[: oc.value], st
+    raise CapacityError("sihsort_perm: capacity retry failed", 0)
+
+
+def sihsort_perm_loopback(inputs: list[torch.Tensor], cfg: SihConfig | None = None, capacity: int | None = None):
+    """sihsort_perm over P logical ranks on ONE GPU (loopback world). Returns (list of per-rank
+    keys, list of per-rank global indices (int64), list of SihStats)."""
+    P = len(inputs)
+    if P < 1:
+        raise InvalidArgument("world: rank count must be >= 1")
+    dt = inputs[0].dtype
+    for t in inputs:
+        _dev(t, "sihsort_perm_loopback")
+        if t.dtype != dt:
+            raise InvalidArgument("sihsort_perm_loopback: all ranks need one dtype")
+    s = _suffix(inputs[0])
+    dev = inputs[0].device.index or 0
+    total = sum(t.numel() for t in inputs)
+    cap = capacity if capacity is not None else total + 1024
+    outs = [torch.empty(cap, dtype=dt, device=inputs[0].device) for _ in range(P)]
+    idxs = [torch.empty(cap, dtype=torch.int64, device=inputs[0].device) for _ in range(P)]
+    in_p = (_P * P)(*[t.data_ptr() for t in inputs])
+    out_p = (_P * P)(*[t.data_ptr() for t in outs])
+    idx_p = (_P * P)(*[t.data_ptr() for t in idxs])
+    ns = (_U64 * P)(*[t.numel() for t in inputs])
+    caps = (_U64 * P)(*[cap] * P)
+    oc = (_U64 * P)()
+    stats = (SihStats * P)()
+    cfg = cfg or SihConfig()
+    fn = _fn(f"ak_sihsort_perm_loopback_{s}", [C.c_int, _U64, _P, _P, _P, _P, _P, _P, C.POINTER(SihConfig), _P])
+    _check(fn(dev, P, C.cast(in_p, _P), C.cast(ns, _P), C.cast(out_p, _P), C.cast(idx_p, _P), C.cast(caps, _P),
+              C.cast(oc, _P), C.byref(cfg), C.cast(stats, _P)), max(oc) if P else 0)
+    return ([outs[r][: oc[r]] for r in range(P)], [idxs[r][: oc[r]] for r in range(P)],
+            [stats[r] for r in range(P)])
+
+
 _DTYPE_CODE = {np.dtype(np.int32): 2, np.dtype(np.int64): 3, np.dtype(np.float32): 5,
                np.dtype(np.float64): 6, np.dtype(np.uint64): 7, np.dtype(np.uint32): 8}
 

@@ -375,6 +375,73 @@ void redistribute_impl(ak_ctx* c, ak_comm* comm, const T* d, uint64_t n, const T
 }
 
 template <typename T>
+void sihsort_perm_impl(ak_ctx* c, ak_comm* comm, const T* in, std::uint64_t n, T* out, std::uint64_t* out_idx,
+                       std::uint64_t cap, std::uint64_t* out_count, const ak_sih_config* cfg, ak_sih_stats* stats) {
+    ctx_lock g(c);
+    need(out_count != nullptr, "sihsort_perm: null out_count");
+    need(n == 0 || in, "sihsort_perm: null input");
+    need(cap == 0 || (out && out_idx), "sihsort_perm: null output");
+    self_comm self;
+    akb::comm_iface& cm = comm_of(comm, self, c);
+    akb::sih_stats_c st{};
+    try {
+        *out_count = akb::sihsort_perm_device<T>(c, cm, in, n, out, out_idx, cap, to_cfg(cfg), st);
+    } catch (const akb::proto_capacity_error& e) {
+        *out_count = e.required;
+        throw;
+    }
+    to_stats(st, stats);
+    akb::ctx_finish(c);
+}
+
+// P logical ranks of the distributed sortperm on one device (threads over the loopback world).
+template <typename T>
+void sihsort_perm_loopback_impl(int device, std::uint64_t P, const T* const* in, const std::uint64_t* n,
+                                T* const* out, std::uint64_t* const* out_idx, const std::uint64_t* cap,
+                                std::uint64_t* out_count, const ak_sih_config* cfg, ak_sih_stats* stats) {
+    need(P >= 1, "world: rank count must be >= 1");
+    need(in && n && out && out_idx && cap && out_count, "sihsort_perm_loopback: null argument");
+    akb::loopback_world world(static_cast<int>(P));
+    std::vector<std::thread> threads;
+    std::mutex err_mu;
+    std::exception_ptr first;
+    const akb::sih_config_c c = to_cfg(cfg);
+    for (std::uint64_t r = 0; r < P; ++r) {
+        threads.emplace_back([&, r] {
+            ak_ctx* ctx = nullptr;
+            try {
+                if (ak_ctx_create(device, nullptr, &ctx) != AK_OK) throw akb::cuda_error(g_err);
+                akb::loopback_comm cm(&world, static_cast<int>(r), ctx->stream);
+                cm.bind(ctx->stream, ctx->sm_count);
+                akb::sih_stats_c st{};
+                {
+                    std::lock_guard<std::mutex> lk(ctx->mu);
+                    AKB_CUDA(cudaSetDevice(device));
+                    try {
+                        out_count[r] =
+                            akb::sihsort_perm_device<T>(ctx, cm, in[r], n[r], out[r], out_idx[r], cap[r], c, st);
+                    } catch (const akb::proto_capacity_error& e) {
+                        out_count[r] = e.required;
+                        throw;
+                    }
+                    AKB_CUDA(cudaStreamSynchronize(ctx->stream));
+                }
+                to_stats(st, stats ? stats + r : nullptr);
+            } catch (...) {
+                {
+                    std::lock_guard<std::mutex> lk(err_mu);
+                    if (!first) first = std::current_exception();
+                }
+                world.abort();
+            }
+            if (ctx) ak_ctx_destroy(ctx);
+        });
+    }
+    for (auto& t : threads) t.join();
+    if (first) std::rethrow_exception(first);
+}
+
+template <typename T>
 void sihsort_loopback_impl(int device, std::uint64_t P, const T* const* in, const std::uint64_t* n,
                            T* const* out, const std::uint64_t* cap, std::uint64_t* out_count,
                            const ak_sih_config* cfg, ak_sih_stats* stats) {
@@ -749,6 +816,15 @@ uint64_t ak_sort_ctx_bytes(uint64_t n, int kb) {
                                 T* const* out, const uint64_t* cap, uint64_t* oc,                       \
                                 const ak_sih_config* cfg, ak_sih_stats* st) {                           \
         return guard([&] { sihsort_loopback_impl<T>(dev, P, in, n, out, cap, oc, cfg, st); });           \
+    }                                                                                                    \
+    int ak_sihsort_perm_##S(ak_ctx* c, ak_comm* cm, const T* in, uint64_t n, T* out, uint64_t* idx,      \
+                            uint64_t cap, uint64_t* oc, const ak_sih_config* cfg, ak_sih_stats* st) {   \
+        return guard([&] { sihsort_perm_impl<T>(c, cm, in, n, out, idx, cap, oc, cfg, st); });           \
+    }                                                                                                    \
+    int ak_sihsort_perm_loopback_##S(int dev, uint64_t P, const T* const* in, const uint64_t* n,        \
+                                     T* const* out, uint64_t* const* idx, const uint64_t* cap,          \
+                                     uint64_t* oc, const ak_sih_config* cfg, ak_sih_stats* st) {        \
+        return guard([&] { sihsort_perm_loopback_impl<T>(dev, P, in, n, out, idx, cap, oc, cfg, st); }); \
     }                                                                                                    \
     int ak_sample_local_##S(ak_ctx* c, const T* d, uint64_t n, uint64_t k, T* h, uint64_t* cnt) {        \
         return guard([&] { sample_local_impl<T>(c, d, n, k, h, cnt); });                                \

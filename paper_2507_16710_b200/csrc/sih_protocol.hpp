@@ -448,6 +448,14 @@ void count_exchange(comm_iface& comm, Local& L, const std::vector<T>& spl, std::
     }
 }
 
+// A rank policy may opt out of the fused pull-merge (bool peer_merge() const): the
+// payload-carrying distributed sortperm exchanges first, then sorts its received runs.
+template <typename Local>
+bool peer_merge_ok(const Local& L) {
+    if constexpr (requires { L.peer_merge(); }) return L.peer_merge();
+    else return true;
+}
+
 // The whole per-rank protocol (sihsort.hpp:508-559).
 template <typename T, typename Local>
 void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_c& st,
@@ -531,7 +539,7 @@ void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_
     // merge reads every incoming run straight from its source rank (the all-to-all fused into
     // the merge: no copy through a receive buffer); otherwise the runs are exchanged first
     std::vector<const void*> peers;
-    if (P > 1 && comm.map_peers(L.sorted_buffer(), peers)) {
+    if (P > 1 && peer_merge_ok(L) && comm.map_peers(L.sorted_buffer(), peers)) {
         st.output_count = L.merge_from_peers(peers, mat);
         comm.peers_released();
     } else {

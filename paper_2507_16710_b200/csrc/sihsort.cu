@@ -656,6 +656,134 @@ struct device_local {
     }
 };
 
+__global__ void iota_u64_kernel(std::uint64_t* __restrict__ out, std::uint64_t n, std::uint64_t base) {
+    const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+    for (std::uint64_t i = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = base + i;
+}
+
+// Distributed sortperm (new work: the reference sihsort is keys-only,
+// sihsort.hpp:472-501): the SIHSort protocol over (key, global index) pairs. Local sort #1
+// is the stable by-key radix sort of (key, offset + i); splitters, refinement and the count
+// exchange run on the keys exactly as for sihsort; the exchange moves keys and indices; the
+// second local sort is the stable by-key sort of the received runs concatenated in
+// source-rank order (sihsort.hpp:555 sorts again too), so ties keep ascending global index:
+// the ranks' outputs concatenated are the globally STABLE sort order and its permutation.
+template <typename T>
+struct device_local_perm {
+    ak_ctx* c;
+    const T* d_in;
+    std::uint64_t n;
+    T* d_out;
+    std::uint64_t* d_idx;
+    std::uint64_t cap;
+    std::size_t P, me;
+    std::uint64_t offset;  // global index of this rank's first key
+    T* sorted = nullptr;
+    std::uint64_t* sidx = nullptr;
+    T* X = nullptr;
+    std::uint64_t* XV = nullptr;
+    T* R = nullptr;
+    std::uint64_t* RV = nullptr;
+    bool direct = false;
+    std::vector<std::uint64_t> roff;
+    std::uint64_t payload_bytes = 0;  // index bytes sent to other ranks
+
+    bool peer_merge() const { return false; }
+    std::uint64_t size() const { return n; }
+    std::uint64_t capacity() const { return cap; }
+
+    void sort_local() {
+        direct = (P == 1 && cap >= n);
+        const std::uint64_t xn = std::max<std::uint64_t>(n, cap);
+        std::size_t need = arena::need(xn * sizeof(T)) + arena::need(xn * 8) + 512;
+        if (!direct)
+            need += arena::need(n * sizeof(T)) + arena::need(n * 8) + arena::need(cap * sizeof(T)) +
+                    arena::need(cap * 8) + 1024;
+        ctx_reserve_aux(c, need);
+        arena a{static_cast<char*>(c->aux), c->aux_bytes};
+        X = a.take<T>(xn);
+        XV = a.take<std::uint64_t>(xn);
+        if (!direct) {
+            sorted = a.take<T>(n);
+            sidx = a.take<std::uint64_t>(n);
+            R = a.take<T>(cap);
+            RV = a.take<std::uint64_t>(cap);
+        } else {
+            sorted = d_out;
+            sidx = d_idx;
+        }
+        if (n == 0) return;
+        iota_u64_kernel<<<static_cast<unsigned>(std::min<std::uint64_t>(ceil_div(n, 256), 4096)), 256, 0, c->stream>>>(
+            sidx, n, offset);
+        AKB_CUDA(cudaGetLastError());
+        c->kernel_launches += 1;
+        radix_sort<T, std::uint64_t>(c, SORT_PAIRS, d_in, sorted, X, sidx, sidx, XV, n, false, true);
+    }
+
+    void samples(std::uint64_t k, std::vector<T>& s, T& front, T& back) {
+        T* dev = reinterpret_cast<T*>(ctx_split(c, k + 2));
+        k = gather_samples<T>(c, sorted, n, k, dev);
+        T* h = static_cast<T*>(ctx_pinned(c, (k + 2) * sizeof(T)));
+        AKB_CUDA(cudaMemcpyAsync(h, dev, (k + 2) * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+        AKB_CUDA(cudaStreamSynchronize(c->stream));
+        front = h[0];
+        back = h[1];
+        s.assign(h + 2, h + 2 + k);
+    }
+
+    void upper_bounds(const std::vector<T>& v, std::vector<std::uint64_t>& out) {
+        device_upper_bounds<T>(c, sorted, n, v, out);
+    }
+
+    const void* sorted_buffer() const { return sorted; }
+
+    void exchange(comm_iface& comm, const std::vector<std::uint64_t>& bounds,
+                  const std::vector<std::uint64_t>& recv_counts) {
+        roff.assign(P, 0);
+        std::uint64_t o = 0;
+        for (std::size_t s = 0; s < P; ++s) {
+            roff[s] = o;
+            if (s != me) o += recv_counts[s];
+        }
+        if (P == 1) return;
+        std::vector<std::uint64_t> soff(P), scnt(P);
+        for (std::size_t d = 0; d < P; ++d) {
+            soff[d] = bounds[d];
+            scnt[d] = bounds[d + 1] - bounds[d];
+            if (d != me) payload_bytes += scnt[d] * sizeof(std::uint64_t);
+        }
+        const int tok = ctx_prof_begin(c, KF_EXCHANGE);
+        comm.exchange(sorted, soff.data(), scnt.data(), R, roff.data(), recv_counts.data(), sizeof(T));
+        comm.exchange(sidx, soff.data(), scnt.data(), RV, roff.data(), recv_counts.data(), sizeof(std::uint64_t));
+        ctx_prof_end(c, tok);
+    }
+
+    std::uint64_t merge_from_peers(const std::vector<const void*>&, const std::vector<std::uint64_t>&) {
+        throw invalid_argument("sihsort_perm: no pull-merge for payload sorts");
+    }
+
+    // local sort #2: the runs concatenated in source-rank order, then the stable by-key sort
+    std::uint64_t merge_runs(const std::vector<std::uint64_t>& bounds,
+                             const std::vector<std::uint64_t>& recv_counts) {
+        if (direct) return n;
+        std::uint64_t total = 0;
+        for (std::size_t s = 0; s < P; ++s) {
+            const std::uint64_t len = recv_counts[s];
+            if (len) {
+                const T* pk = s == me ? sorted + bounds[me] : R + roff[s];
+                const std::uint64_t* pv = s == me ? sidx + bounds[me] : RV + roff[s];
+                AKB_CUDA(cudaMemcpyAsync(d_out + total, pk, len * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+                AKB_CUDA(cudaMemcpyAsync(d_idx + total, pv, len * 8, cudaMemcpyDeviceToDevice, c->stream));
+            }
+            total += len;
+        }
+        if (total > 1)
+            radix_sort<T, std::uint64_t>(c, SORT_PAIRS, d_out, d_out, X, d_idx, d_idx, XV, total, false, true);
+        return total;
+    }
+};
+
 }  // namespace
 
 template <typename T>
@@ -667,6 +795,25 @@ std::uint64_t sihsort_device(ak_ctx* c, comm_iface& comm, const T* d_in, std::ui
     sihsort_run<T>(comm, L, cfg, st, splitters);
     if (L.pulled_bytes)
         if (auto* ic = dynamic_cast<ipc_comm*>(&comm)) ic->add_pulled(L.pulled_bytes);
+    return st.output_count;
+}
+
+template <typename T>
+std::uint64_t sihsort_perm_device(ak_ctx* c, comm_iface& comm, const T* d_in, std::uint64_t n, T* d_out,
+                                  std::uint64_t* d_idx, std::uint64_t cap, const sih_config_c& cfg,
+                                  sih_stats_c& st) {
+    const std::size_t P = static_cast<std::size_t>(comm.size());
+    const std::size_t me = static_cast<std::size_t>(comm.rank());
+    // global index offsets: one control allgather of the per-rank counts (not a collective of
+    // the reference's accounting, like the count exchange)
+    std::vector<std::uint64_t> all(P);
+    comm.allgather(&n, sizeof(n), all.data());
+    std::uint64_t offset = 0;
+    for (std::size_t r = 0; r < me; ++r) offset += all[r];
+    device_local_perm<T> L{c, d_in, n, d_out, d_idx, cap, P, me, offset};
+    sihsort_run<T>(comm, L, cfg, st);
+    st.redistribution_bytes += L.payload_bytes;
+    comm.ctr.p2p_bytes += L.payload_bytes;
     return st.output_count;
 }
 
@@ -748,6 +895,9 @@ std::uint64_t redistribute_device(ak_ctx* c, comm_iface& comm, const T* sorted, 
     template std::uint64_t sihsort_device<T>(ak_ctx*, comm_iface&, const T*, std::uint64_t, T*,      \
                                              std::uint64_t, const sih_config_c&, sih_stats_c&,      \
                                              std::vector<T>*);                                      \
+    template std::uint64_t sihsort_perm_device<T>(ak_ctx*, comm_iface&, const T*, std::uint64_t, T*,  \
+                                                  std::uint64_t*, std::uint64_t, const sih_config_c&,   \
+                                                  sih_stats_c&);                                        \
     template std::uint64_t sample_local_device<T>(ak_ctx*, const T*, std::uint64_t, std::uint64_t, T*); \
     template refine_out refine_device<T>(ak_ctx*, comm_iface&, const T*, std::uint64_t, std::vector<T>&,  \
                                          const sih_config_c&);                                          \

@@ -148,6 +148,14 @@ std::uint64_t sihsort_device(ak_ctx* c, comm_iface& comm, const T* d_in, std::ui
                              std::uint64_t cap, const sih_config_c& cfg, sih_stats_c& st,
                              std::vector<T>* splitters = nullptr);
 
+// Distributed sortperm (new; the reference sihsort is keys-only): d_out / d_idx (capacity cap)
+// = this rank's slice of the globally stable order of all ranks' keys, as keys and their
+// global indices (rank r's key i has global index sum_{q<r} n_q + i).
+template <typename T>
+std::uint64_t sihsort_perm_device(ak_ctx* c, comm_iface& comm, const T* d_in, std::uint64_t n, T* d_out,
+                                  std::uint64_t* d_idx, std::uint64_t cap, const sih_config_c& cfg,
+                                  sih_stats_c& st);
+
 // Public stage functions (sihsort.hpp:264-501) over a caller's sorted device keys.
 template <typename T>
 std::uint64_t sample_local_device(ak_ctx* c, const T* sorted, std::uint64_t n, std::uint64_t k, T* host_out);

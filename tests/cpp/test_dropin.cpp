@@ -289,6 +289,28 @@ void test_sihsort() {
     }
 }
 
+void test_sihsort_perm() {  // the distributed sortperm extension: stable global order + permutation
+    // P=2, [5,1,5] and [1,5,0] -> global keys [5,1,5,1,5,0]; stable order: 0@5, 1@1, 1@3, 5@0, 5@2, 5@4
+    ak::sim::world w(2);
+    std::vector<std::vector<float>> keys(2);
+    std::vector<std::vector<std::uint64_t>> idx(2);
+    ak::sim::run_ranks(w, [&](ak::sim::rank_comm& comm) {
+        const auto r = comm.rank();
+        const auto e = ak::exec_backend::cuda();
+        std::vector<float> mine = r == 0 ? std::vector<float>{5, 1, 5} : std::vector<float>{1, 5, 0};
+        auto [k, i, st] = ak::sihsort_perm<float>(std::span<const float>(mine), comm, ak::sih_config{}, e);
+        keys[r] = k;
+        idx[r] = i;
+    });
+    std::vector<float> ck;
+    std::vector<std::uint64_t> ci;
+    for (int r = 0; r < 2; ++r) {
+        ck.insert(ck.end(), keys[r].begin(), keys[r].end());
+        ci.insert(ci.end(), idx[r].begin(), idx[r].end());
+    }
+    CHECK(ck == (std::vector<float>{0, 1, 1, 5, 5, 5}));
+    CHECK(ci == (std::vector<std::uint64_t>{5, 1, 3, 0, 2, 4}));
+}
 
 void test_sihsort_stages() {  // SPEC.md:282-325 known answers for the stage functions
     const std::vector<std::int64_t> ten{1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
@@ -469,7 +491,7 @@ int main() {
     const std::pair<const char*, void (*)()> tests[] = {
         {"partition", test_partition}, {"reduce", test_reduce},     {"accumulate", test_accumulate},
         {"search", test_search},       {"sort", test_sort},         {"sortperm", test_sortperm},
-        {"sihsort", test_sihsort},     {"sihsort_stages", test_sihsort_stages},
+        {"sihsort", test_sihsort},     {"sihsort_perm", test_sihsort_perm},     {"sihsort_stages", test_sihsort_stages},
         {"rank_comm", test_rank_comm}, {"predicates", test_predicates},
         {"distributed", test_distributed_reduce_scan}};
     for (const auto& [name, fn] : tests) {

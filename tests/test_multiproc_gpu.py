@@ -36,7 +36,7 @@ def gpu_count():
     return torch.cuda.device_count()
 
 
-def worker(rank, world, port, transport, n, dtype, outdir, same_gpu):
+def worker(rank, world, port, transport, n, dtype, outdir, same_gpu, op="sort"):
     sys.path.insert(0, ROOT)
     import torch
     import torch.distributed as dist
@@ -61,6 +61,13 @@ def worker(rank, world, port, transport, n, dtype, outdir, same_gpu):
     d = torch.from_numpy(x.view(np.int64) if dt == np.uint64 else x).to(f"cuda:{dev}")
     if dt == np.uint64:
         d = d.view(torch.uint64)
+    if op == "perm":  # distributed sortperm: keys + global indices over the same transport
+        k, i, st = ak.sihsort_perm(d, comm, None, ex)
+        np.savez(os.path.join(outdir, f"r{rank}.npz"), keys=k.cpu().numpy(), idx=i.cpu().numpy())
+        comm.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     outs = []
     for _ in range(2):  # twice: the second call reuses the cached peer mappings
         out, st = ak.sihsort(d, comm, None, ex)
@@ -73,10 +80,10 @@ def worker(rank, world, port, transport, n, dtype, outdir, same_gpu):
     dist.destroy_process_group()
 
 
-def run_world(transport, world, n, dtype, same_gpu):
+def run_world(transport, world, n, dtype, same_gpu, op="sort"):
     import torch.multiprocessing as mp
     with tempfile.TemporaryDirectory() as d:
-        mp.start_processes(worker, args=(world, free_port(), transport, n, dtype, d, same_gpu), nprocs=world,
+        mp.start_processes(worker, args=(world, free_port(), transport, n, dtype, d, same_gpu, op), nprocs=world,
                            join=True, start_method="spawn")
         return [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(world)]
 
@@ -103,6 +110,18 @@ def test_ipc_exchange_processes_on_one_gpu(orc, world, n, dtype):
         pytest.skip("oracle/_ref not built")
     res = run_world("ipc", world, n, dtype, same_gpu=True)
     check_vs_reference(orc, res, world, n, dtype)
+
+
+def test_ipc_distributed_sortperm_processes_on_one_gpu(orc):
+    """sihsort_perm over IpcComm with 3 processes: keys AND global indices travel through the
+    peer-store exchange; the concatenated outputs are the stable global order."""
+    world, n = 3, 200_000
+    res = run_world("ipc", world, n, np.int64, same_gpu=True, op="perm")
+    ins = [orc.ref_bench_keys(42, r, n + 17 * r, np.dtype(np.int64)) for r in range(world)]
+    allk = np.concatenate(ins)
+    perm = np.argsort(allk, kind="stable")
+    assert np.array_equal(np.concatenate([res[r]["idx"] for r in range(world)]), perm)
+    assert np.array_equal(np.concatenate([res[r]["keys"] for r in range(world)]), allk[perm])
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
