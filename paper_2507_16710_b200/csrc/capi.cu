@@ -162,7 +162,10 @@ void sortperm_impl(ak_ctx* c, const T* data, std::uint64_t n, I* out, std::uint6
         // 32-bit integer keys: composite (key, index) keys through the 64-bit hybrid sort
         // (1e8 i32: 2.31 ms vs 2.64 ms onesweep). Float keys keep the onesweep: their
         // exponent-heavy top bits need a third MSD level, which costs more than it saves
-        // (1e8 f32 uniform in [-1e6, 1e6): 3.03 ms vs 2.64 ms, measured r01).
+        // (1e8 f32 uniform in [-1e6, 1e6): 3.03 ms vs 2.64 ms, measured r01; r02 with the
+        // current kernels 3.51 ms vs 2.72 ms: 3 MSD levels 1.11 + histograms 0.57 + compose /
+        // decompose 0.52 + counting stage 0.95 ms, whose ranges span many tiny low-exponent
+        // buckets).
         if constexpr (sizeof(T) == 4 && std::is_integral_v<T>)
             done = akb::sortperm_composite<T, V>(c, data, n, reinterpret_cast<V*>(out), desc != 0);
         if (!done)
