@@ -2447,13 +2447,16 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
         if (big_local && !bucket_mode) step = LB_CAP / 2;  // provisional (re-cut from the exact largest bucket)
         J = bucket_mode ? (1ull << (8 * m)) : ceil_div(n, step);
         base_id = prefix << (8 * m);
-        hist_scan_kernel<<<PASSES, RADIX, 0, c->stream>>>(g_hist, g_offs);
-        AKB_CUDA(cudaGetLastError());
-        c->kernel_launches += 1;
         const T* cur = kin;
         const bool tma_ok = (reinterpret_cast<std::uintptr_t>(kin) & 15) == 0 &&
                             (reinterpret_cast<std::uintptr_t>(kalt) & 15) == 0;  // TMA-fed passes
-        if (joint_valid && (m == 2 || m == 3) && top == PASSES && tma_ok && n < (std::uint64_t(1) << 32)) {
+        const bool msd_path = joint_valid && (m == 2 || m == 3) && top == PASSES && tma_ok && n < (std::uint64_t(1) << 32);
+        if (!msd_path) {  // the onesweep passes and the one-pass bucket cuts read the digit offsets
+            hist_scan_kernel<<<PASSES, RADIX, 0, c->stream>>>(g_hist, g_offs);
+            AKB_CUDA(cudaGetLastError());
+            c->kernel_launches += 1;
+        }
+        if (msd_path) {
             // unstable MSD partition by the top 16 (24) bits (keys-only integers: order among
             // equal keys is unobservable). Measured and dropped (r02): two levels of 11 + 9 bits
             // instead of three 8-bit ones at n >= 2^29 -- 2^30 int64 MSD 11.9 ms vs 12.1 ms: the

@@ -489,11 +489,19 @@ void sihsort_run(comm_iface& comm, Local& L, const sih_config_c& cfg, sih_stats_
     mine.n = n;
     if (n > 0) {
         const std::uint64_t k = std::min<std::uint64_t>(spr, n);
-        L.samples(k, samples, mine.data_min, mine.data_max);
-        mine.samples = samples.size();
-        if (!samples.empty()) {
-            mine.sample_min = samples.front();
-            mine.sample_max = samples.back();
+        if (P > 1) {
+            L.samples(k, samples, mine.data_min, mine.data_max);
+            mine.samples = samples.size();
+            if (!samples.empty()) {
+                mine.sample_min = samples.front();
+                mine.sample_max = samples.back();
+            }
+        } else {
+            // one rank: select_splitters returns P - 1 = 0 splitters and refine stops before
+            // reading the bounds, so the sample VALUES are never used; only their count enters
+            // the protocol (the histogram allreduce happens iff samples exist). The device
+            // gather and its host round trip are skipped.
+            mine.samples = k;
         }
     }
     const proto::summary<T> g = proto::global_summary(comm, mine);
