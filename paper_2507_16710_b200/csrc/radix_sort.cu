@@ -2352,9 +2352,12 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                             n >= (std::uint64_t(1) << 24);  // below: the joint-histogram flush dominates
         msdbuf = msd_ok ? ctx_msd(c) : nullptr;
         bool joint_valid = false;
-        // below 2^29 keys the plan needs only digits 7 and 6 (the joint histogram's marginals):
-        // the joint read skips digit 5, and a plan that does reach it re-reads (skewed keys)
-        const bool d5 = n >= (std::uint64_t(1) << 29);
+        // up to ~2^30 keys the plan needs only digits 7 and 6 (the joint histogram's marginals:
+        // two MSD levels, then the 4608-key or the big-range stage): the joint read skips digit
+        // 5, and a plan that does reach it re-reads (skewed keys). Above, uniform keys need a
+        // third level, so the first read counts digit 5 too.
+        const bool d5 = AKB_CFG_BIG_LOCAL ? n > (std::uint64_t(1) << 30) + (std::uint64_t(1) << 26)
+                                          : n >= (std::uint64_t(1) << 29);
         if (msd_ok && !d5) first = PASSES - 2;
         auto run_hist = [&](int f) {
             if (f != 0 && msd_ok) {
