@@ -970,15 +970,6 @@ __device__ __forceinline__ void local_radix_range(const T* __restrict__ in, T* _
     for (std::uint32_t j = tid; j < len; j += LOCAL_BLOCK) out[b + j] = s_stage[j];
 }
 
-// One CTA per range.
-template <typename T, int ITEMS>
-__global__ void __launch_bounds__(LOCAL_BLOCK, ITEMS <= 8 ? 4 : (ITEMS <= 12 ? 3 : 2))
-    local_sort_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
-                      int desc, int low, std::uint64_t* big) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    local_radix_range<T, ITEMS>(in, out, cuts, blockIdx.x, desc, low, big, smem);
-}
-
 // Persistent loop over the ranges listed in list[1 .. list[0]] (the ranges the counting
 // kernel below handed back).
 template <typename T, int ITEMS>
@@ -1975,19 +1966,6 @@ constexpr int msd_env() { return AKB_CFG_MSD; }
 #endif
 constexpr int hybrid_env() { return AKB_CFG_HYBRID; }
 
-template <typename T, int ITEMS>
-void launch_local(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc, int low,
-                  std::uint64_t* big) {
-    using LS = local_smem<T, ITEMS>;
-    smem_attr(c, local_sort_kernel<T, ITEMS>, LS::total);
-    const int tok = ctx_prof_begin(c, KF_LOCAL);
-    local_sort_kernel<T, ITEMS><<<static_cast<unsigned>(J), LOCAL_BLOCK, LS::total, c->stream>>>(
-        G, kout, cuts, desc ? 1 : 0, low, big);
-    AKB_CUDA(cudaGetLastError());
-    ctx_prof_end(c, tok);
-    c->kernel_launches += 1;
-}
-
 // ---------------------------------------------------------------------------
 // Keys-only 64-bit integer P-way merge (SIHSort's second local step): the output is cut
 // into value tiles [b_j, b_{j+1}) (b_j from a sorted sample of every run); tile j is the
@@ -2137,12 +2115,6 @@ __global__ void mc_maxtile_kernel(const std::uint64_t* __restrict__ pos, int P, 
     }
     if ((threadIdx.x & 31) == 0 && t) atomicMax(mx, static_cast<unsigned long long>(t));
 }
-
-// 0: stable radix local stage for every range (experiment builds: make variant DEFS=-DAKB_CFG_LOCAL_COUNT=...)
-#ifndef AKB_CFG_LOCAL_COUNT
-#define AKB_CFG_LOCAL_COUNT 1
-#endif
-constexpr int local_count_env() { return AKB_CFG_LOCAL_COUNT; }
 
 // Counting local stage (integer keys only), then the stable radix kernel over the ranges
 // it handed back (persistent loop over redo[1 .. redo[0]]; no host round trip).
@@ -2439,7 +2411,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
             } else {
                 // ranges of several buckets: cap them at 12-item CTAs (4608 keys), whose
                 // counting kernel keeps two CTAs per SM (16-item ones fit only one)
-                const bool counting = std::is_integral_v<T> && local_count_env() != 0 && need <= LOCAL_BLOCK * 6;
+                const bool counting = need <= LOCAL_BLOCK * 6;
                 if (counting) items = 12;
                 step = static_cast<std::uint64_t>((counting ? LOCAL_BLOCK * 12 : LOCAL_TILE) - need);
                 if (step < 256) step = 256;
@@ -2538,22 +2510,12 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
 #ifdef AKB_CFG_LOCAL_LOW
     low = AKB_CFG_LOCAL_LOW;
 #endif
-    bool counted = false;
-    if constexpr (std::is_integral_v<T> && sizeof(T) == 8) {  // the only keys that reach here (see above)
-        if (big_local) {
-            launch_local_big<T>(c, G, kout, cuts, J, desc, !bucket_mode, big);
-            counted = true;
-        } else if (local_count_env() != 0) {
-            if (items == 8) launch_local_count<T, 8>(c, G, kout, cuts, J, n, desc, low, big, redo);
-            else if (items == 12) launch_local_count<T, 12>(c, G, kout, cuts, J, n, desc, low, big, redo);
-            else launch_local_count<T, 16>(c, G, kout, cuts, J, n, desc, low, big, redo);
-            counted = true;
-        }
-    }
-    if (counted) {
-    } else if (items == 8) launch_local<T, 8>(c, G, kout, cuts, J, desc, low, big);
-    else if (items == 12) launch_local<T, 12>(c, G, kout, cuts, J, desc, low, big);
-    else launch_local<T, 16>(c, G, kout, cuts, J, desc, low, big);
+    // the counting stages (64-bit integer keys are the only ones that reach here, see above);
+    // ranges they hand back run the stable on-chip radix (local_redo_kernel)
+    if (big_local) launch_local_big<T>(c, G, kout, cuts, J, desc, !bucket_mode, big);
+    else if (items == 8) launch_local_count<T, 8>(c, G, kout, cuts, J, n, desc, low, big, redo);
+    else if (items == 12) launch_local_count<T, 12>(c, G, kout, cuts, J, n, desc, low, big, redo);
+    else launch_local_count<T, 16>(c, G, kout, cuts, J, n, desc, low, big, redo);
     if (m == 0) return true;  // a single range of <= LOCAL_TILE keys always fits
     // oversized ranges (skewed keys): plain LSD on each such segment, or on the whole
     // array when there are many (every range is a stable permutation of its keys, equal
