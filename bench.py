@@ -13,8 +13,9 @@ bench.cpp:164-173), weak scaling, one rank per GPU, NCCL between GPUs.
 A step = one full ak.sihsort (local radix sort, sampling, splitters, refinement,
 NCCL all-to-all-v, P-way merge) of device-resident input into a device output.
 `e2e` = the same with every step's input copied host->device from pinned memory and
-its output copied back (steps pipelined over two buffer sets: step i+1's upload
-overlaps step i's download on the full-duplex PCIe link); `e2e.blocking` = one
+its output copied back (steps pipelined over two buffer sets: step i+1's upload is
+enqueued before step i's sort and overlaps it and step i-1's download on the full-duplex
+PCIe link); `e2e.blocking` = one
 blocking host-buffer C-ABI call per step (ak_sihsort_host_*: H2D + sort + D2H).
 
 At N=1 the line also carries `configs`: every other BASELINE.json config measured on
@@ -665,13 +666,16 @@ def run_e2e(args, ak, torch, np, ex, comm, cfg, h_in, n, t_dt, dev, barrier, wor
         e.record(down)
     counts = [0, 0]
 
-    def pipe_step(i):
-        b = i % 2
-        with torch.cuda.stream(up):  # d_in2[b] is free: step i-2's (blocking) sort has returned
+    def upload(j):  # d_in2[j % 2] is free: step j - 2's (blocking) sort has returned
+        b = j % 2
+        with torch.cuda.stream(up):
             d_in2[b].copy_(h_in, non_blocking=True)
             ev_up[b].record(up)
+
+    def sort_and_download(j):
+        b = j % 2
         ex.stream.wait_event(ev_up[b])
-        ex.stream.wait_event(ev_down[b])  # d_out2[b] is free once step i-2's download is done
+        ex.stream.wait_event(ev_down[b])  # d_out2[b] is free once step j - 2's download is done
         with torch.cuda.stream(ex.stream):
             res, _ = ak.sihsort(d_in2[b], comm, cfg, ex, out=d_out2[b], capacity=cap)
         counts[b] = res.numel()
@@ -680,15 +684,21 @@ def run_e2e(args, ak, torch, np, ex, comm, cfg, h_in, n, t_dt, dev, barrier, wor
             h_out2[b][:counts[b]].copy_(d_out2[b][:counts[b]], non_blocking=True)
             ev_down[b].record(down)
 
-    for i in range(2):  # warm-up
-        pipe_step(i)
+    def run(steps):
+        # step i + 1's upload is enqueued before step i's (blocking) sort, so the upload stream
+        # stays busy while step i sorts and step i - 1's output downloads
+        upload(0)
+        for i in range(steps):
+            if i + 1 < steps:
+                upload(i + 1)
+            sort_and_download(i)
+
+    run(2)  # warm-up
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(up)
-    d2h = 0
-    for i in range(k):
-        pipe_step(i)
-        d2h += counts[i % 2] * 8
+    run(k)
+    d2h = sum(counts[i % 2] * 8 for i in range(k))
     e1.record(down)
     barrier()
     pipe_ms = e0.elapsed_time(e1) / k
@@ -717,8 +727,9 @@ def run_e2e(args, ak, torch, np, ex, comm, cfg, h_in, n, t_dt, dev, barrier, wor
     return {"value": world * n * 8 / 1e9 / (pipe_ms / 1e3), "unit": "GB/s", "h2d_bytes_per_step": n * 8,
             "d2h_bytes_per_step": d2h // k, "ms_per_step": pipe_ms, "steps": k, "output_copy_check": ok,
             "how": "public API ak.sihsort on device buffers; every step copies its input from pinned host memory "
-                   "(upload stream) and its output back (download stream); two buffer sets, so step i+1's "
-                   "upload overlaps step i's download (PCIe is full duplex)",
+                   "(upload stream) and its output back (download stream); two buffer sets: step i+1's upload "
+                   "is enqueued before step i's sort, so it overlaps that sort and step i-1's download (PCIe "
+                   "is full duplex)",
             "blocking": {"value": world * n * 8 / 1e9 / (blk_ms / 1e3), "ms_per_step": blk_ms, "steps": kb,
                          "how": "one blocking C-ABI call per step (ak_sihsort_host_*): H2D + sort + D2H"}}
 
