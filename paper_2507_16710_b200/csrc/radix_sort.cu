@@ -1586,9 +1586,9 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
 // 144 KB of shared memory; 18 keys per thread of 1024 in registers), so two partition levels suffice
 // where the 4608-key stage needed a third level and its 24-bit histogram. The algorithm is
 // local_count3's (up to 2^15 packed u16 bins, one shared atomic per key, scan, bin-order
-// scatter, per-position rank); the differences: bins over the offset to the range's minimum
-// (min / max reduction: a range of several buckets may straddle an aligned boundary, where
-// OR-reduced varying bits would put nearly every key in a few bins), the single buffer (the
+// scatter, per-position rank; ranges = aligned groups of 1, 2, 4 or 8 16-bit buckets, so the
+// OR-reduced varying bits are exact -- a range cut at arbitrary bucket boundaries could
+// straddle an aligned boundary and crowd a few bins); the differences: the single buffer (the
 // next range's TMA copy is issued once this range's rank loop is done) and the scan over up
 // to 16384 counter words. A bin over LC_MAX_BIN keys sends the range to the segment fallback
 // (big list: the stable redo kernel holds only 6144 keys).
@@ -1608,7 +1608,7 @@ struct lb_smem {
     static constexpr std::size_t buf_off = 0;
     static constexpr std::size_t cnt_off = buf_bytes;
     static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LB_WORDS + 4);
-    static constexpr std::size_t red_off = cnt_off + cnt_bytes;                 // 2 x WARPS x u64 (min, max)
+    static constexpr std::size_t red_off = cnt_off + cnt_bytes;                 // WARPS x u64 (+ spare)
     static constexpr std::size_t wsum_off = red_off + 2 * LB_WARPS * sizeof(std::uint64_t);
     static constexpr std::size_t bar_off = wsum_off + LB_WARPS * sizeof(std::uint32_t);
     static constexpr std::size_t total = bar_off + sizeof(std::uint64_t);
@@ -1668,7 +1668,7 @@ __device__ __forceinline__ void lb_scan_counts(std::uint32_t* s_cw, std::uint32_
     if (tid == 0) reinterpret_cast<std::uint16_t*>(s_cw)[2 * nwords] = static_cast<std::uint16_t>(len);
 }
 
-template <typename T, bool DESC, bool MINMAX>
+template <typename T, bool DESC>
 __global__ void __launch_bounds__(LB_BLOCK, 1)
     local_big_kernel(const T* __restrict__ in, T* out, const std::uint64_t* __restrict__ cuts, std::uint64_t J,
                      std::uint64_t* big) {
@@ -1712,7 +1712,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
         const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
         B* sb = reinterpret_cast<B*>(smem + L::buf_off) + static_cast<std::uint32_t>(b & 1);
         B k[ITEMS];
-        B mn = ~B(0), mx = 0;
+        B mx = 0;  // OR of the bits that differ from the first key
         if (ok_range) {
             mbar_wait(s_bar, phase);
             phase ^= 1u;
@@ -1723,30 +1723,12 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
                 const std::uint32_t li = static_cast<std::uint32_t>(i * LB_BLOCK + tid);
                 const B v = (li < len ? sb[li] : k0) ^ X;  // padding repeats key 0 (neutral)
                 k[i] = v;
-                if constexpr (MINMAX) {
-                    mn = v < mn ? v : mn;
-                    mx = v > mx ? v : mx;
-                } else {
-                    mx |= v ^ (k0 ^ X);  // OR of the bits that differ from key 0
-                }
+                mx |= v ^ (k0 ^ X);
             }
         }
-        if constexpr (MINMAX) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const B a = __shfl_xor_sync(FULL, mn, o), z = __shfl_xor_sync(FULL, mx, o);
-                mn = a < mn ? a : mn;
-                mx = z > mx ? z : mx;
-            }
-            if (lane == 0) {
-                s_red[warp] = mn;
-                s_red[LB_WARPS + warp] = mx;
-            }
-        } else {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx |= __shfl_xor_sync(FULL, mx, o);
-            if (lane == 0) s_red[warp] = mx;
-        }
+        for (int o = 16; o > 0; o >>= 1) mx |= __shfl_xor_sync(FULL, mx, o);
+        if (lane == 0) s_red[warp] = mx;
         const int nb_want = min(LB_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
         const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
         if (nwords_w >= 4) {
@@ -1760,26 +1742,11 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
             const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
             big[1 + slot] = r;
         }
-        B vary = 0, kmin = 0;
-        if (!done) {
-            // lanes 0-15 fold the minima, 16-31 the maxima: bins over the offset to the range's
-            // minimum (a range of several buckets may straddle an aligned boundary)
-            // (!MINMAX: OR of the differing bits -- ranges of one aligned bucket -- and kmin = 0)
-            if constexpr (MINMAX) {
-                B a = lane < LB_WARPS ? s_red[lane] : ~B(0), z = lane < LB_WARPS ? s_red[LB_WARPS + lane] : B(0);
+        B vary = 0;
+        if (!done) {  // ranges are aligned groups of buckets: the OR of the differing bits is exact
+            vary = lane < LB_WARPS ? s_red[lane] : B(0);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const B a2 = __shfl_xor_sync(FULL, a, o), z2 = __shfl_xor_sync(FULL, z, o);
-                    a = a2 < a ? a2 : a;
-                    z = z2 > z ? z2 : z;
-                }
-                kmin = a;
-                vary = z - a;
-            } else {
-                vary = lane < LB_WARPS ? s_red[lane] : B(0);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
-            }
+            for (int o = 16; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
             if (vary == 0) {  // every key equal
                 if (copy_equal)
                     for (std::uint32_t j = tid; j < len; j += LB_BLOCK) out[b + j] = static_cast<T>(k[0] ^ X);
@@ -1796,13 +1763,8 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
             std::uint32_t sl[SW];
 #pragma unroll
             for (int w = 0; w < SW; ++w) sl[w] = 0;
-            if constexpr (MINMAX) {
-#pragma unroll
-                for (int i = 0; i < ITEMS; ++i) k[i] -= kmin;  // offsets from here on (order kept)
-            }
             bool over = false;
-            // item rows past len are skipped by block-uniform branches (ranges of several
-            // buckets are ~half full at 2^29)
+            // item rows past len are skipped by block-uniform branches
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 if (static_cast<std::uint32_t>(i * LB_BLOCK) >= len) break;
@@ -1831,7 +1793,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
                 }
                 __syncthreads();
                 lc_rank_store<B, LB_BLOCK>(sb, s_c16, len, B(0), shift, bmask,
-                                 [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>((v + kmin) ^ X); });
+                                 [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>(v ^ X); });
             }
         }
         // the buffer and the counters are idle once every thread is here: next range's copy
@@ -1927,10 +1889,10 @@ __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, i
 
 // cuts[0] = 0, cuts[j] = ends[j - 1] (the MSD cursors after the last pass = bucket ends), cuts[J] = n.
 __global__ void cuts_from_ends_kernel(const std::uint64_t* __restrict__ ends, std::uint64_t J, std::uint64_t n,
-                                      std::uint64_t* __restrict__ cuts) {
+                                      std::uint64_t group, std::uint64_t* __restrict__ cuts) {
     const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j > J) return;
-    cuts[j] = j == 0 ? 0 : (j == J ? n : ends[j - 1]);
+    cuts[j] = j == 0 ? 0 : (j == J ? n : ends[j * group - 1]);
 }
 
 // cut b = first index whose top bits are >= b (bucket starts), b in [0, J); cuts[J] = n.
@@ -2187,14 +2149,11 @@ void sort_oversized(ak_ctx* c, const T* G, T* kout, T* kalt, std::uint64_t n, bo
 #define AKB_CFG_BIG_LOCAL 1
 #endif
 
-// minmax: ranges of several buckets (bins over the offset to the minimum); otherwise every
-// range is one aligned bucket (OR-reduced varying bits, cheaper)
 template <typename T>
 void launch_local_big(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc,
-                      bool minmax, std::uint64_t* big) {
+                      std::uint64_t* big) {
     using LB = lb_smem<T>;
-    auto kern = minmax ? (desc ? local_big_kernel<T, true, true> : local_big_kernel<T, false, true>)
-                       : (desc ? local_big_kernel<T, true, false> : local_big_kernel<T, false, false>);
+    auto kern = desc ? local_big_kernel<T, true> : local_big_kernel<T, false>;
     smem_attr(c, kern, LB::total);
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     kern<<<static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count))), LB_BLOCK,
@@ -2310,6 +2269,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
     int m = 0, top = PASSES, items = LOCAL_MAX_ITEMS;
     bool bucket_mode = false, big_local = false;
+    std::uint64_t group = 1;  // big-range stage: 16-bit buckets per range
     std::uint64_t step = n, J = 1, base_id = 0;
     const T* G = kin;  // buffer holding the bucket-ordered keys
     std::uint64_t* msdbuf = nullptr;
@@ -2399,7 +2359,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                 // 16-bit buckets over the 4608-key stage but within LB_CAP: two MSD levels + the
                 // big-range stage instead of a third level (see local_big_kernel)
                 big_local = true;
-                bucket_mode = est >= 0.55 * LB_CAP;
+                bucket_mode = true;  // groups of 2^g buckets per range, g from the exact largest bucket
                 break;
             }
             if (need > LOCAL_TILE) continue;
@@ -2419,7 +2379,6 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
             break;
         }
         if (m > 3 || m > top) return false;
-        if (big_local && !bucket_mode) step = LB_CAP / 2;  // provisional (re-cut from the exact largest bucket)
         J = bucket_mode ? (1ull << (8 * m)) : ceil_div(n, step);
         base_id = prefix << (8 * m);
         const T* cur = kin;
@@ -2443,13 +2402,16 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                 msd_level3<T>(c, kout, kalt, n, desc);
                 cur = kalt;
             }
-            if (big_local && !bucket_mode) {
+            if (big_local) {
+                // ranges = groups of `group` consecutive 16-bit buckets (aligned: OR-reduced
+                // varying bits stay exact), group * largest bucket <= LB_CAP
                 const std::uint64_t maxb = msd_max_bucket(c, m);
                 if (maxb + 256 <= static_cast<std::uint64_t>(LB_CAP)) {
-                    step = LB_CAP - maxb;
-                    J = ceil_div(n, step);
+                    while (group < 8 && 2 * group * maxb <= static_cast<std::uint64_t>(LB_CAP)) group *= 2;
+                    J = 65536 / group;
                 } else {  // a bucket over the big-range stage (skewed keys): a third level instead
                     big_local = false;
+                    bucket_mode = false;
                     msd_level3<T>(c, kout, kalt, n, desc);
                     cur = kalt;
                     m = 3;
@@ -2486,15 +2448,15 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     std::uint64_t* redo = big + J + 1;
     AKB_CUDA(cudaMemsetAsync(big, 0, sizeof(std::uint64_t), c->stream));
     const int top_shift = 8 * (top - (m > 0 ? m : 1));
-    if (bucket_mode && used_msd && m == 2 && J == 65536)
-        // the MSD cursors end at the bucket ends: cuts[j] = end of bucket j - 1 (no search)
+    if (bucket_mode && used_msd && m == 2 && J * group == 65536)
+        // the MSD cursors end at the bucket ends: cuts[j] = end of bucket j * group - 1 (no search)
         cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(msdbuf + 65536, J, n,
-                                                                                                 cuts);
+                                                                                                 group, cuts);
     else if (bucket_mode && !used_msd && m == 1 && J == RADIX)
         // one onesweep pass over digit top - 1: bucket j starts at that digit's exclusive
         // global offset j (hist_scan_kernel), so cuts[j] = offs[j] (no search)
         cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
-            g_offs + (top - 1) * RADIX + 1, J, n, cuts);
+            g_offs + (top - 1) * RADIX + 1, J, n, 1, cuts);
     else if (bucket_mode)
         bucket_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
             G, n, top_shift, desc ? 1 : 0, J, base_id, cuts);
@@ -2512,7 +2474,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
 #endif
     // the counting stages (64-bit integer keys are the only ones that reach here, see above);
     // ranges they hand back run the stable on-chip radix (local_redo_kernel)
-    if (big_local) launch_local_big<T>(c, G, kout, cuts, J, desc, !bucket_mode, big);
+    if (big_local) launch_local_big<T>(c, G, kout, cuts, J, desc, big);
     else if (items == 8) launch_local_count<T, 8>(c, G, kout, cuts, J, n, desc, low, big, redo);
     else if (items == 12) launch_local_count<T, 12>(c, G, kout, cuts, J, n, desc, low, big, redo);
     else launch_local_count<T, 16>(c, G, kout, cuts, J, n, desc, low, big, redo);

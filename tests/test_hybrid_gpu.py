@@ -153,8 +153,8 @@ def test_small_sort_graph_replays(ak, ex, dev, n):
 @pytest.mark.parametrize("n,kind", [((1 << 29) + 12345, "uniform"), ((1 << 29) + 7, "dups"), (1 << 30, "uniform")])
 def test_hybrid_big_range_stage(ak, ex, dev, n, kind):
     """n >= 2^29: partitions by the top 8 and 16 bits, then the big-range counting stage
-    (local_big_kernel: whole 16-bit buckets of up to 18432 keys; range mode with min / max
-    bins at 2^29, one bucket per range at 2^30). Checked by sortedness + order-independent
+    (local_big_kernel: ranges of up to 18432 keys = aligned groups of 16-bit buckets, two
+    per range at 2^29, one at 2^30). Checked by sortedness + order-independent
     multiset fingerprint (a full host sort of 8 GiB is too slow)."""
     g = torch.Generator(device=dev)
     g.manual_seed(n)
@@ -185,8 +185,7 @@ def _top13(rng, n, low):
 @pytest.mark.parametrize("kind", ["uniform", "dups", "const", "narrow", "oversized"])
 @pytest.mark.parametrize("desc", [False, True])
 def test_big_range_stage_skew(ak, ex, dev, kind, desc):
-    """local_big_kernel at 2^26 in range mode (ranges of one or two ~8K-key buckets, bins over
-    the offset to the range minimum) under skew: uniform, dups (bins over 48 keys: the
+    """local_big_kernel at 2^26 (ranges = aligned pairs of ~8K-key 16-bit buckets) under skew: uniform, dups (bins over 48 keys: the
     segment fallback), const (every 16-bit bucket one value), narrow (60 % of each bucket in
     a 2^30-wide sliver), oversized (one top-13 value holds 40000 keys: a bucket over 18432
     keys, so the plan falls back to a third MSD level and the 4608-key stage)."""
