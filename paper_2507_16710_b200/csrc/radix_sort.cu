@@ -2422,12 +2422,19 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
                     J = ceil_div(n, step);
                 }
             } else if (!bucket_mode) {
-                // ranges of several buckets: size them from the exact largest bucket (the
-                // plan's estimate assumes independent digits, which skewed keys -- e.g. the
-                // exponent-heavy top bits of composite float keys -- violate)
+                // ranges of several buckets, sized from the exact largest bucket (the plan's
+                // estimate assumes independent digits, which skewed keys -- e.g. the
+                // exponent-heavy top bits of composite float keys -- violate). Two levels:
+                // aligned groups of 2^g 16-bit buckets (2^g x largest bucket <= the CTA's
+                // capacity), so the counting stage's OR-reduced varying bits stay exact and
+                // ranges stay nearly full; three levels: step-cut ranges of several buckets.
                 const std::uint64_t maxb = msd_max_bucket(c, m);
                 const std::uint64_t cap = static_cast<std::uint64_t>(LOCAL_BLOCK) * items;
-                if (maxb + 256 <= cap) {
+                if (m == 2 && maxb > 0 && maxb <= cap) {
+                    while (group < 256 && 2 * group * maxb <= cap) group *= 2;
+                    bucket_mode = true;
+                    J = 65536 / group;
+                } else if (maxb + 256 <= cap) {
                     step = cap - maxb;
                     J = ceil_div(n, step);
                 }
