@@ -508,12 +508,20 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     AKB_PHASE(3);
 
     // ---- stage keys (and payload) in shared memory in digit order ----
+    // 4-byte keys with 4-byte payload: one packed 8-byte pair per slot (one store and one load
+    // per element instead of two each)
+    constexpr bool PACK = L::HAS_KEYS_SMEM && L::HAS_VALS && sizeof(T) == 4 && sizeof(V) == 4;
+    uint2* s_pairs = reinterpret_cast<uint2*>(smem + L::keys_off);
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const std::uint32_t d = (dg[i / 4] >> (8 * (i % 4))) & 0xffu;
         const std::uint32_t pos = wh[d] + ((rk[i / 2] >> (16 * (i % 2))) & 0xffffu);
-        if constexpr (L::HAS_KEYS_SMEM) s_keys[pos] = k[i];
-        if constexpr (L::HAS_VALS) s_vals[pos] = v[i];
+        if constexpr (PACK) {
+            s_pairs[pos] = make_uint2(__builtin_bit_cast(std::uint32_t, k[i]), static_cast<std::uint32_t>(v[i]));
+        } else {
+            if constexpr (L::HAS_KEYS_SMEM) s_keys[pos] = k[i];
+            if constexpr (L::HAS_VALS) s_vals[pos] = v[i];
+        }
     }
 
     // ---- windowed decoupled look-back for this tile's per-digit exclusive prefix ----
@@ -563,7 +571,19 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
             if constexpr (NARROW) return static_cast<std::uint32_t>(s_gofs32[d] + j);
             else return s_gofs[d] + j;
         };
-        if constexpr (MODE == SORT_LOWMEM) {
+        if constexpr (PACK) {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const std::uint32_t j = i * BLOCK + tid;
+                if (F || j < valid) {
+                    const uint2 pr = s_pairs[j];
+                    const T key = __builtin_bit_cast(T, pr.x);
+                    const std::uint64_t o = dst(digit_of(key, shift, dsc), j);
+                    if constexpr (WK) kout[o] = key;
+                    vout[o] = static_cast<V>(pr.y);
+                }
+            }
+        } else if constexpr (MODE == SORT_LOWMEM) {
             // only the index array moves; the digit of staged slot j is recomputed
             // from data[index] (L1/L2 hit: just gathered by this tile)
 #pragma unroll
