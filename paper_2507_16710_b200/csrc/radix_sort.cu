@@ -38,6 +38,9 @@ constexpr std::uint32_t FULL = 0xffffffffu;
 #ifndef AKB_OS_ITEMS
 #define AKB_OS_ITEMS 16  // keys per thread of a keys-only pass tile
 #endif
+#ifndef AKB_OS_PAIR_ITEMS
+#define AKB_OS_PAIR_ITEMS 16  // elements per thread of a 4 + 4-byte (key, payload) pass tile
+#endif
 #ifndef AKB_OS_BLOCK
 #define AKB_OS_BLOCK 384  // threads per pass CTA (>= RADIX)
 #endif
@@ -77,7 +80,7 @@ struct tile_cfg {
     static constexpr int BLOCK = AKB_OS_BLOCK;
     static constexpr bool HAS_VALS = MODE != SORT_KEYS;
     static constexpr int ITEMS =
-        !HAS_VALS ? AKB_OS_ITEMS : (sizeof(T) + sizeof(V) <= 8 ? 16 : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
+        !HAS_VALS ? AKB_OS_ITEMS : (sizeof(T) + sizeof(V) <= 8 ? AKB_OS_PAIR_ITEMS : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
     static constexpr int TILE = BLOCK * ITEMS;
     static constexpr int MIN_BLOCKS = AKB_OS_MINB;
 };
