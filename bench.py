@@ -459,13 +459,23 @@ def main():
 
     import paper_2507_16710_b200 as ak
 
+    # AKB_BENCH_SHARE_GPU=1 (test mode, tests/test_multiproc_gpu.py): every rank on device 0,
+    # control over gloo and the IPC transport (NCCL refuses two ranks on one device), so the
+    # N > 1 code path of this script runs on a one-GPU box; its numbers are not a measurement
+    share = world > 1 and os.environ.get("AKB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+        args.transport = "ipc"
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     pg = None
     comm = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
         if args.transport == "ipc":
             comm = ak.IpcComm(local)
@@ -542,14 +552,15 @@ def main():
     fp_in, fp_out = fingerprint(d_in), fingerprint(out)
     if comm is not None:
         import torch.distributed as dist
-        tot = torch.tensor([fp_in[0], fp_out[0]], dtype=torch.int64, device=dev)
+        cdev = "cpu" if share else dev  # gloo: host tensors
+        tot = torch.tensor([fp_in[0], fp_out[0]], dtype=torch.int64, device=cdev)
         dist.all_reduce(tot)
-        sums = torch.tensor([[fp_in[1], fp_in[2], fp_out[1], fp_out[2]]], dtype=torch.int64, device=dev)
+        sums = torch.tensor([[fp_in[1], fp_in[2], fp_out[1], fp_out[2]]], dtype=torch.int64, device=cdev)
         gathered = [torch.empty_like(sums) for _ in range(world)]
         dist.all_gather(gathered, sums)
         g = [sum(int(v) for v in col) % (1 << 64) for col in torch.cat(gathered).cpu().numpy().T]
         multiset_ok = bool(tot[0].item() == tot[1].item() and g[0] == g[2] and g[1] == g[3])
-        ok_t = torch.tensor([1 if sorted_ok else 0], device=dev)
+        ok_t = torch.tensor([1 if sorted_ok else 0], device=cdev)
         dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
         sorted_ok = bool(ok_t.item())
     else:
@@ -583,7 +594,8 @@ def main():
     tr = ncu_traffic(dom)
     names = {"msd": "msd_pass_kernel (unstable top-digit partition pass over all keys; per-bin atomic cursors)",
              "onesweep": "onesweep_kernel (one 8-bit digit pass over all keys)",
-             "local": "local_count_kernel (on-chip counting sort of every bucket range; TMA-fed, persistent)",
+             "local": "counting stage (local_count3_kernel: <= 4608-key bucket ranges, 2 CTAs/SM; local_big_kernel: "
+                      "<= 18432-key ranges at 2^29-2^30, 1 CTA/SM; on-chip counting sort, TMA-fed, persistent)",
              "hist": "hist_kernel (top-digit histograms)"}
     roofline = None
     if dom:
@@ -615,6 +627,8 @@ def main():
         "gpu_launches": gpu_launches,
         "clocks": clocks,
     }
+    if share:
+        line["config"]["test_mode"] = "AKB_BENCH_SHARE_GPU: every rank on GPU 0 (code-path test, not a measurement)"
     if world > 1 and fam["exchange"][1]:
         ex_ms = fam["exchange"][0] / fam["exchange"][1]
         sent = sent_per_step

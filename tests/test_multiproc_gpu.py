@@ -165,6 +165,24 @@ def test_two_devices_in_one_process(ak, orc):
     assert not errs
 
 
+@pytest.mark.parametrize("nproc", [2, 3])
+def test_torchrun_bench_ranks_sharing_one_gpu(nproc):
+    """bench.py's N > 1 path (torchrun, max-over-ranks timing, cross-rank checks, the nvlink
+    and e2e objects) with every rank on GPU 0 over the IPC transport (AKB_BENCH_SHARE_GPU=1):
+    what the driver's multi-GPU runs execute, runnable on a one-GPU box."""
+    env = dict(os.environ, AKB_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+                        "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.join(ROOT, "bench.py"),
+                        "--gpus", str(nproc), "--steps", "2", "--warmup", "3", "--log2n", "22"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == nproc and line["config"]["global_keys"] == nproc << 22
+    assert line["config"]["sorted_check"] and line["config"]["multiset_fingerprint_check"]
+    assert line["nvlink"]["bytes_sent_per_gpu"] > 0 and line["e2e"]["output_copy_check"]
+    assert "test_mode" in line["config"]
+
+
 @pytest.mark.parametrize("transport", ["nccl", "ipc"])
 def test_torchrun_bench_two_gpus(transport):
     if gpu_count() < 2:
