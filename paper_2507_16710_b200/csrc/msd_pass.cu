@@ -119,11 +119,21 @@ __global__ void __launch_bounds__(1024) joint_scan_a_kernel(const std::uint64_t*
                                                             std::uint64_t* __restrict__ cur16,
                                                             std::uint64_t* __restrict__ sums,
                                                             std::uint64_t* __restrict__ colpart,
-                                                            std::uint64_t* __restrict__ g_hist) {
+                                                            std::uint64_t* __restrict__ g_hist,
+                                                            unsigned long long* __restrict__ maxslot) {
     __shared__ std::uint64_t s_w[32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int i = blockIdx.x * 1024 + t;
     const std::uint64_t v = g_joint[i];
+    {  // the largest 16-bit bucket (device plans): warp max, one atomic per warp
+        std::uint64_t m = v;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const std::uint64_t y = __shfl_xor_sync(FULLM, m, o);
+            m = m > y ? m : y;
+        }
+        if (lane == 0 && m) atomicMax(maxslot, static_cast<unsigned long long>(m));
+    }
     std::uint64_t inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -233,9 +243,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL L > 1 = the 8L-bit prefixes
     // of the (already 8(L-1)-bit partitioned) tile, relative to its first key's 8(L-1)-bit
     // prefix (cursor index = the 8L-bit prefix)
-    if constexpr (LEVEL == 0) {
-        if (plan[0] != 0) return;
-    }
+    if (plan != nullptr && plan[0] != 0) return;  // device plan: not applicable, nothing written
     using G = mp_level<LEVEL>;
     constexpr int DB = G::DB;
     const int TOP = LEVEL == 0 ? plan[1] : G::TOP;  // shift of the digit (cursor index = key >> TOP)
@@ -506,7 +514,9 @@ void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t
 void msd_joint_scan(ak_ctx* c, std::uint64_t* g_joint, std::uint64_t* g_hist) {
     std::uint64_t* sums = g_joint + 2 * JOINT_BINS + 256 + 8;  // ctx_msd tail
     std::uint64_t* colpart = sums + JS_CTAS;
-    joint_scan_a_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, sums, colpart, g_hist);
+    auto* maxslot = reinterpret_cast<unsigned long long*>(g_joint + 2 * JOINT_BINS + 256 + 1);
+    AKB_CUDA(cudaMemsetAsync(maxslot, 0, sizeof(std::uint64_t), c->stream));
+    joint_scan_a_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint, g_joint + JOINT_BINS, sums, colpart, g_hist, maxslot);
     joint_scan_b_kernel<<<JS_CTAS, 1024, 0, c->stream>>>(g_joint + JOINT_BINS, g_joint + 2 * JOINT_BINS, sums, colpart,
                                                          g_hist);
     AKB_CUDA(cudaGetLastError());
@@ -515,16 +525,16 @@ void msd_joint_scan(ak_ctx* c, std::uint64_t* g_joint, std::uint64_t* g_hist) {
 
 template <typename T>
 void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool desc, const std::uint64_t* g_joint,
-               std::uint64_t* cur16, std::uint64_t* cur8) {
+               std::uint64_t* cur16, std::uint64_t* cur8, const int* plan) {
     smem_attr(c, msd_pass_kernel<T, 1>, mp_smem::total);
     smem_attr(c, msd_pass_kernel<T, 2>, mp_smem::total);
     const unsigned tiles = static_cast<unsigned>(ceil_div(n, MP_TILE));
     int tok = ctx_prof_begin(c, KF_MSD);
-    msd_pass_kernel<T, 1><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kmid, n, desc ? 1 : 0, cur8);
+    msd_pass_kernel<T, 1><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kin, kmid, n, desc ? 1 : 0, cur8, plan);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     tok = ctx_prof_begin(c, KF_MSD);
-    msd_pass_kernel<T, 2><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kmid, kout, n, desc ? 1 : 0, cur16);
+    msd_pass_kernel<T, 2><<<tiles, MP_BLOCK, mp_smem::total, c->stream>>>(kmid, kout, n, desc ? 1 : 0, cur16, plan);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     c->kernel_launches += 2;
@@ -610,8 +620,8 @@ template void msd_hist<std::int64_t>(ak_ctx*, const std::int64_t*, std::uint64_t
 template void msd_hist<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t, bool, std::uint64_t*,
                                       std::uint64_t*, bool);
 template void msd_top16<std::int64_t>(ak_ctx*, const std::int64_t*, std::int64_t*, std::int64_t*, std::uint64_t,
-                                      bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*);
+                                      bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*, const int*);
 template void msd_top16<std::uint64_t>(ak_ctx*, const std::uint64_t*, std::uint64_t*, std::uint64_t*, std::uint64_t,
-                                       bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*);
+                                       bool, const std::uint64_t*, std::uint64_t*, std::uint64_t*, const int*);
 
 }  // namespace akb

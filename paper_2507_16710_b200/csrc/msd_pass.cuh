@@ -23,9 +23,13 @@ void msd_joint_scan(ak_ctx* c, std::uint64_t* g_joint, std::uint64_t* g_hist);
 
 // Two partition passes (kin -> kmid by the top 8 bits, kmid -> kout by the top 16 bits);
 // afterwards kout is ordered by its top 16 bits (order inside a 16-bit bucket arbitrary).
+// plan (device, optional): plan[0] != 0 -> both passes return without writing.
 template <typename T>
 void msd_top16(ak_ctx* c, const T* kin, T* kmid, T* kout, std::uint64_t n, bool desc, const std::uint64_t* g_joint,
-               std::uint64_t* cur16, std::uint64_t* cur8);
+               std::uint64_t* cur16, std::uint64_t* cur8, const int* plan = nullptr);
+
+// The largest 16-bit bucket of the last msd_hist (device slot, filled by its joint scan).
+inline std::uint64_t* msd_joint_max_slot(std::uint64_t* g_joint) { return g_joint + 2 * 65536 + 256 + 1; }
 
 // Third partition level (n >= 2^29): kin (ordered by its top 16 bits) -> kout ordered by
 // its top 24 bits; the 24-bit histogram is built by an extra read of kin (tiles span few

@@ -1468,7 +1468,8 @@ __device__ __forceinline__ void lc_rank_store(const B* sb, const std::uint16_t* 
 template <typename T, int ITEMS, bool DESC>
 __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
     local_count3_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
-                        std::uint64_t J, std::uint64_t* big, std::uint64_t* redo) {
+                        std::uint64_t J, std::uint64_t* big, std::uint64_t* redo,
+                        const std::uint64_t* __restrict__ dplan) {
     using L = lc3_smem<T, ITEMS>;
     using B = typename key_traits<T>::bits;
     constexpr int CAP = L::CAP;
@@ -1496,7 +1497,8 @@ __global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
         mbar_init_fence();
     }
     __syncthreads();
-    const std::uint32_t nr = static_cast<std::uint32_t>(J);  // ranges < 2^32 (n / 256 at most)
+    // ranges < 2^32 (n / 256 at most); a device plan (dplan: {mode, group, J}) overrides J
+    const std::uint32_t nr = static_cast<std::uint32_t>(dplan ? (dplan[0] ? 0 : dplan[2]) : J);
     if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x, 0);
     std::uint32_t phase = 0;  // bit q = parity of buffer q's next completion
     const bool copy_equal = in != out;
@@ -1694,7 +1696,7 @@ __device__ __forceinline__ void lb_scan_counts(std::uint32_t* s_cw, std::uint32_
 template <typename T, bool DESC>
 __global__ void __launch_bounds__(LB_BLOCK, 1)
     local_big_kernel(const T* __restrict__ in, T* out, const std::uint64_t* __restrict__ cuts, std::uint64_t J,
-                     std::uint64_t* big) {
+                     std::uint64_t* big, const std::uint64_t* __restrict__ dplan) {
     using L = lb_smem<T>;
     using B = typename key_traits<T>::bits;
     constexpr int ITEMS = LB_ITEMS;
@@ -1723,7 +1725,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
         mbar_init_fence();
     }
     __syncthreads();
-    const std::uint32_t nr = static_cast<std::uint32_t>(J);
+    const std::uint32_t nr = static_cast<std::uint32_t>(dplan ? (dplan[0] ? 0 : dplan[2]) : J);
     if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x);
     std::uint32_t phase = 0;
     const bool copy_equal = in != out;
@@ -1912,7 +1914,13 @@ __global__ void range_cuts_kernel(const T* __restrict__ keys, std::uint64_t n, i
 
 // cuts[0] = 0, cuts[j] = ends[j - 1] (the MSD cursors after the last pass = bucket ends), cuts[J] = n.
 __global__ void cuts_from_ends_kernel(const std::uint64_t* __restrict__ ends, std::uint64_t J, std::uint64_t n,
-                                      std::uint64_t group, std::uint64_t* __restrict__ cuts) {
+                                      std::uint64_t group, const std::uint64_t* __restrict__ dplan,
+                                      std::uint64_t* __restrict__ cuts) {
+    if (dplan) {  // device plan {mode, group, J}: nothing to cut when the plan does not apply
+        if (dplan[0]) return;
+        group = dplan[1];
+        J = dplan[2];
+    }
     const std::uint64_t j = static_cast<std::uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j > J) return;
     cuts[j] = j == 0 ? 0 : (j == J ? n : ends[j * group - 1]);
@@ -2105,7 +2113,8 @@ __global__ void mc_maxtile_kernel(const std::uint64_t* __restrict__ pos, int P, 
 // it handed back (persistent loop over redo[1 .. redo[0]]; no host round trip).
 template <typename T, int ITEMS>
 void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, std::uint64_t n,
-                        bool desc, int low, std::uint64_t* big, std::uint64_t* redo, bool redo_zeroed = false) {
+                        bool desc, int low, std::uint64_t* big, std::uint64_t* redo, bool redo_zeroed = false,
+                        const std::uint64_t* dplan = nullptr) {
     constexpr int CITEMS = ITEMS * LOCAL_BLOCK / LC_BLOCK;
     static_assert(CITEMS * LC_BLOCK == ITEMS * LOCAL_BLOCK, "same range capacity");
     using CS = lc_smem<T, CITEMS>;
@@ -2120,7 +2129,7 @@ void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cut
             static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * C3::MINB));
         auto kern = desc ? local_count3_kernel<T, CITEMS, true> : local_count3_kernel<T, CITEMS, false>;
         smem_attr(c, kern, C3::total);
-        kern<<<grid3, LC_BLOCK, C3::total, c->stream>>>(G, kout, cuts, J, big, redo);
+        kern<<<grid3, LC_BLOCK, C3::total, c->stream>>>(G, kout, cuts, J, big, redo, dplan);
     } else {
         auto kern = desc ? local_count_kernel<T, CITEMS, true> : local_count_kernel<T, CITEMS, false>;
         smem_attr(c, kern, CS::total);
@@ -2174,13 +2183,13 @@ void sort_oversized(ak_ctx* c, const T* G, T* kout, T* kalt, std::uint64_t n, bo
 
 template <typename T>
 void launch_local_big(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts, std::uint64_t J, bool desc,
-                      std::uint64_t* big) {
+                      std::uint64_t* big, const std::uint64_t* dplan = nullptr) {
     using LB = lb_smem<T>;
     auto kern = desc ? local_big_kernel<T, true> : local_big_kernel<T, false>;
     smem_attr(c, kern, LB::total);
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     kern<<<static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count))), LB_BLOCK,
-           LB::total, c->stream>>>(G, kout, cuts, J, big);
+           LB::total, c->stream>>>(G, kout, cuts, J, big, dplan);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     c->kernel_launches += 1;
@@ -2274,6 +2283,64 @@ bool small_sort_device(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t 
     return true;
 }
 
+// Device plan of a two-level sort (2^24 <= n <= ~2^30; no host round trip before the last
+// kernel): the largest 16-bit bucket (filled by the joint scan) picks how many aligned
+// buckets form one range of the predicted counting stage, or rejects the plan (mode 1: the
+// partition passes, the cuts and the counting stage then do nothing, and the host plan runs
+// from the same histograms). dplan = {mode, group, J}.
+__global__ void two_level_plan_kernel(const std::uint64_t* __restrict__ maxslot, std::uint64_t fit_cap,
+                                      std::uint64_t group_cap, std::uint64_t max_group,
+                                      std::uint64_t* __restrict__ dplan) {
+    const std::uint64_t maxb = *maxslot;
+    std::uint64_t mode = 1, g = 1;
+    if (maxb > 0 && maxb <= fit_cap) {
+        mode = 0;
+        while (g < max_group && 2 * g * maxb <= group_cap) g *= 2;
+    }
+    dplan[0] = mode;
+    dplan[1] = g;
+    dplan[2] = 65536 / g;
+}
+
+// The device-planned two-level sort: joint histogram -> plan -> two unstable partition passes
+// -> bucket-group cuts -> counting stage (4608-key, or the big-range stage above ~2^28 keys),
+// then ONE synchronisation reading {plan, oversized-range count}. Returns false when the plan
+// was rejected (skewed keys): nothing was written, and the histograms in g_hist / msdbuf are
+// those the host plan starts from.
+template <typename T>
+bool two_level_device(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc, std::uint64_t* g_hist,
+                      std::uint64_t* msdbuf) {
+    constexpr std::uint64_t JM = 65536;
+    const bool big = AKB_CFG_BIG_LOCAL && n > (std::uint64_t(1) << 28) + (std::uint64_t(1) << 23);
+    std::uint64_t* cuts = ctx_cuts(c, 4 * (JM + 1) + 8);
+    std::uint64_t* bigl = cuts + JM + 1;
+    std::uint64_t* redo = bigl + JM + 1;
+    std::uint64_t* dplan = redo + JM + 1;
+    constexpr int ITEMS = 12;  // the 4608-key stage: 2 CTAs per SM
+    const std::uint64_t cap = big ? static_cast<std::uint64_t>(LB_CAP) : static_cast<std::uint64_t>(LOCAL_BLOCK) * ITEMS;
+    AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * 8 * RADIX) * 8 + 8 * 4, c->stream));
+    msd_hist<T>(c, kin, n, desc, g_hist, msdbuf, false);
+    two_level_plan_kernel<<<1, 1, 0, c->stream>>>(msd_joint_max_slot(msdbuf), big ? cap - 256 : cap, cap,
+                                                  big ? 8 : 256, dplan);
+    AKB_CUDA(cudaGetLastError());
+    msd_top16<T>(c, kin, kalt, kout, n, desc, msdbuf, msdbuf + JM, msdbuf + 2 * JM, reinterpret_cast<const int*>(dplan));
+    cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(JM + 1, 256)), 256, 0, c->stream>>>(msdbuf + JM, JM, n, 1,
+                                                                                              dplan, cuts);
+    AKB_CUDA(cudaGetLastError());
+    AKB_CUDA(cudaMemsetAsync(bigl, 0, sizeof(std::uint64_t), c->stream));
+    if (big) launch_local_big<T>(c, kout, kout, cuts, JM, desc, bigl, dplan);
+    else launch_local_count<T, ITEMS>(c, kout, kout, cuts, JM, n, desc, 0, bigl, redo, false, dplan);
+    c->kernel_launches += 2;
+    auto* h = static_cast<std::uint64_t*>(ctx_pinned(c, 4 * sizeof(std::uint64_t)));
+    AKB_CUDA(cudaMemcpyAsync(h, dplan, 3 * sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaMemcpyAsync(h + 3, bigl, sizeof(std::uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    AKB_CUDA(cudaStreamSynchronize(c->stream));  // the call's one synchronisation
+    if (h[0] != 0) return false;
+    const std::uint64_t J = h[2], nbig = h[3];
+    sort_oversized<T>(c, kout, kout, kalt, n, desc, cuts, bigl, J, nbig);
+    return true;
+}
+
 template <typename T>
 bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc) {
     constexpr int PASSES = key_traits<T>::nbits / 8;
@@ -2288,6 +2355,16 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     if (env == 0 || PASSES != 8 || !std::is_integral_v<T>) return false;
     if (n == 0) return true;
     std::uint64_t* g_hist = static_cast<std::uint64_t*>(c->small);
+    // two MSD levels planned on the device (the common case of 2^24 .. ~2^30 keys); a rejected
+    // plan leaves the histograms for the host plan below
+    bool hist_ready = false;
+    if (env < 0 && msd_env() != 0 && n >= (std::uint64_t(1) << 24) &&
+        n <= (std::uint64_t(1) << 30) + (std::uint64_t(1) << 26) &&
+        ((reinterpret_cast<std::uintptr_t>(kin) | reinterpret_cast<std::uintptr_t>(kalt) |
+          reinterpret_cast<std::uintptr_t>(kout)) & 15) == 0) {
+        if (two_level_device<T>(c, kin, kout, kalt, n, desc, g_hist, ctx_msd(c))) return true;
+        hist_ready = true;
+    }
     std::uint64_t* g_offs = g_hist + PASSES * RADIX;
     std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
     int m = 0, top = PASSES, items = LOCAL_MAX_ITEMS;
@@ -2299,7 +2376,7 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     bool used_msd = false;
     if (n > static_cast<std::uint64_t>(LOCAL_TILE)) {
         const int blocks = c->sm_count * 4;
-        AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
+        if (!hist_ready) AKB_CUDA(cudaMemsetAsync(c->small, 0, (2 * PASSES * RADIX) * 8 + PASSES * 4, c->stream));
         int first = PASSES - 3;
         // 64-bit integer keys: the first read also builds the 16-bit joint histogram that
         // the unstable MSD passes start their cursors from
@@ -2327,7 +2404,8 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
             ctx_prof_end(c, tok);
             c->kernel_launches += 1;
         };
-        run_hist(first);
+        if (hist_ready) joint_valid = msd_ok && !d5;  // the device plan's read (digit 5 not counted)
+        else run_hist(first);
         std::vector<std::uint64_t> h(PASSES * RADIX);
         auto fetch = [&] {
             std::uint64_t* hp = static_cast<std::uint64_t*>(ctx_pinned(c, PASSES * RADIX * sizeof(std::uint64_t)));
@@ -2481,12 +2559,12 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     if (bucket_mode && used_msd && m == 2 && J * group == 65536)
         // the MSD cursors end at the bucket ends: cuts[j] = end of bucket j * group - 1 (no search)
         cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(msdbuf + 65536, J, n,
-                                                                                                 group, cuts);
+                                                                                                 group, nullptr, cuts);
     else if (bucket_mode && !used_msd && m == 1 && J == RADIX)
         // one onesweep pass over digit top - 1: bucket j starts at that digit's exclusive
         // global offset j (hist_scan_kernel), so cuts[j] = offs[j] (no search)
         cuts_from_ends_kernel<<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
-            g_offs + (top - 1) * RADIX + 1, J, n, 1, cuts);
+            g_offs + (top - 1) * RADIX + 1, J, n, 1, nullptr, cuts);
     else if (bucket_mode)
         bucket_cuts_kernel<T><<<static_cast<unsigned>(ceil_div(J + 1, 256)), 256, 0, c->stream>>>(
             G, n, top_shift, desc ? 1 : 0, J, base_id, cuts);
