@@ -183,18 +183,22 @@ __global__ void __launch_bounds__(1024) joint_scan_b_kernel(std::uint64_t* __res
     }
 }
 
+// 256 threads x 20 keys (5120-key tiles), 3 CTAs per SM: r02 sweep at 2^28 int64, ms per
+// pass: 512x16 (2 CTAs/SM) 0.954, 256x16 (4) 0.914, 256x18 (3) 0.922, 256x20 (3) 0.891,
+// 256x22 (3) 0.916, 256x24 (3) 0.942, 288x18 (3) 0.898, 320x16 (3) 0.904, 256x12 (5) 1.01,
+// 192x16 (5) 1.62 -- more, smaller CTAs overlap one another's load / claim latencies better
 #ifndef AKB_MP_BLOCK
-#define AKB_MP_BLOCK 512
+#define AKB_MP_BLOCK 256
 #endif
 constexpr int MP_BLOCK = AKB_MP_BLOCK;
 #ifndef AKB_MP_ITEMS
-#define AKB_MP_ITEMS 16
+#define AKB_MP_ITEMS 20
 #endif
 #ifndef AKB_MP_MINB
-#define AKB_MP_MINB 2
+#define AKB_MP_MINB 3
 #endif
 constexpr int MP_ITEMS = AKB_MP_ITEMS;
-constexpr int MP_TILE = MP_BLOCK * MP_ITEMS;  // 8192 keys
+constexpr int MP_TILE = MP_BLOCK * MP_ITEMS;  // 5120 keys
 constexpr int MP_SPAN = 4;                    // LEVEL 2: top buckets a tile may span on chip
 constexpr int MP_BINS = 256 * MP_SPAN;
 #ifndef AKB_MP_PARTS
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     // bin starts: thread t owns whole bins [t*BPT, t*BPT + BPT) (BPT <= 2) and their PARTS
     // sub-counters; exclusive scan in (bin, part) order + one global claim per non-empty bin
     {
-        constexpr int BPTMAX = MP_BINS / MP_BLOCK;  // bins per thread (<= 4)
+        constexpr int BPTMAX = MP_BLOCK >= MP_BINS ? 1 : (2 * MP_BLOCK >= MP_BINS ? 2 : 4);  // bins per thread
         constexpr int MAXC = BPTMAX * MP_PARTS;
         const std::uint32_t bpt = nbins > 2 * MP_BLOCK ? 4u : nbins > MP_BLOCK ? 2u : 1u;
         const std::uint32_t fs = static_cast<std::uint32_t>(tid) * bpt * MP_PARTS;  // first sub-counter
