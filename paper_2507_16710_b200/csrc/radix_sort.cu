@@ -1038,6 +1038,10 @@ __device__ __forceinline__ std::uint32_t lex_less96(std::uint64_t a, std::uint32
 
 constexpr int LC_BLOCK = 512;
 constexpr int LC_WARPS = LC_BLOCK / 32;
+#ifndef AKB_LC3_BLOCK
+#define AKB_LC3_BLOCK 512  // threads of the TMA-fed counting stage (local_count3_kernel)
+#endif
+constexpr int LC3_BLOCK = AKB_LC3_BLOCK;
 constexpr int LC_MAX_BITS = 13;                        // up to 8192 bins (u16 counts, 2 per word)
 constexpr int LC_WORDS = (1 << LC_MAX_BITS) / 2;       // 4096 counter words = 16 KB
 constexpr std::uint32_t LC_MAX_BIN = 48;
@@ -1045,9 +1049,9 @@ constexpr std::uint32_t LC_MAX_BIN = 48;
 #define AKB_LC_EXTRA 1  // bins = 2^(ceil(log2(len)) + EXTRA): ~2 bins per key
 #endif
 
-template <typename T, int ITEMS>
+template <typename T, int ITEMS, int NT = LC_BLOCK>
 struct lc_smem {
-    static constexpr int CAP = LC_BLOCK * ITEMS;
+    static constexpr int CAP = NT * ITEMS;
     // two key buffers (the range being sorted + the next range in flight), each with one
     // spare key at both ends: TMA copies the 16-byte aligned superset of a range
     static constexpr std::size_t buf_bytes = (sizeof(T) * (CAP + 2) + 15) & ~std::size_t(15);
@@ -1063,9 +1067,9 @@ struct lc_smem {
 
 // local_count3_kernel: as lc_smem plus a second counter table (the rank loop of range i still
 // reads its table while a faster warp zeroes the other one for range i + 1: no end barrier).
-template <typename T, int ITEMS>
-struct lc3_smem : lc_smem<T, ITEMS> {
-    using B = lc_smem<T, ITEMS>;
+template <typename T, int ITEMS, int NT = LC_BLOCK>
+struct lc3_smem : lc_smem<T, ITEMS, NT> {
+    using B = lc_smem<T, ITEMS, NT>;
     static constexpr std::size_t cnt2_off = B::total;
     static constexpr std::size_t total = cnt2_off + B::cnt_bytes;
     static constexpr int MINB = total + 1024 <= 114 * 1024 ? 2 : 1;
@@ -1465,192 +1469,20 @@ __device__ __forceinline__ void lc_rank_store(const B* sb, const std::uint16_t* 
     }
 }
 
-template <typename T, int ITEMS, bool DESC>
-__global__ void __launch_bounds__(LC_BLOCK, lc3_smem<T, ITEMS>::MINB)
-    local_count3_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
-                        std::uint64_t J, std::uint64_t* big, std::uint64_t* redo,
-                        const std::uint64_t* __restrict__ dplan) {
-    using L = lc3_smem<T, ITEMS>;
-    using B = typename key_traits<T>::bits;
-    constexpr int CAP = L::CAP;
-    static_assert(sizeof(T) == 8, "8-byte keys");
-    constexpr B X = (std::is_signed_v<T> ? (B(1) << 63) : B(0)) ^ (DESC ? ~B(0) : B(0));  // raw <-> ordered
-    extern __shared__ __align__(16) unsigned char smem[];
-    B* s_red = reinterpret_cast<B*>(smem + L::red_off);  // [2][WARPS] OR partials
-    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
-    std::uint64_t* s_bar = reinterpret_cast<std::uint64_t*>(smem + L::bar_off);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    auto fits = [&](std::uint64_t rb, std::uint64_t re) {
-        return re > rb && re - rb <= static_cast<std::uint64_t>(CAP);
-    };
-    auto issue = [&](std::uint64_t r, int q) {  // one thread
-        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
-        if (!fits(rb, re)) return;
-        const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
-        const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
-        mbar_arrive_expect_tx(s_bar + q, bytes);
-        bulk_g2s(smem + L::buf_off + q * L::buf_bytes, in + a0, bytes, s_bar + q);
-    };
-    if (tid == 0) {
-        mbar_init(s_bar, 1);
-        mbar_init(s_bar + 1, 1);
-        mbar_init_fence();
-    }
-    __syncthreads();
-    // ranges < 2^32 (n / 256 at most); a device plan (dplan: {mode, group, J}) overrides J
-    const std::uint32_t nr = static_cast<std::uint32_t>(dplan ? (dplan[0] ? 0 : dplan[2]) : J);
-    if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x, 0);
-    std::uint32_t phase = 0;  // bit q = parity of buffer q's next completion
-    const bool copy_equal = in != out;
-
-#pragma unroll 1
-    for (std::uint32_t r = blockIdx.x, it = 0; r < nr; r += gridDim.x, ++it) {
-        const int cur = static_cast<int>(it & 1);
-        const std::uint64_t b = cuts[r], e = cuts[r + 1];
-        const bool ok_range = fits(b, e);
-        const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
-        B* sb = reinterpret_cast<B*>(smem + L::buf_off + cur * L::buf_bytes) + static_cast<std::uint32_t>(b & 1);
-        B* red = s_red + cur * LC_WARPS;
-        // packed u16 counts / starts, one table per parity of the range
-        std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + (cur ? L::cnt2_off : L::cnt_off));
-        const std::uint16_t* s_c16 = reinterpret_cast<const std::uint16_t*>(s_cw);
-        B k[ITEMS];
-        B orx = 0;
-        if (ok_range) {
-            mbar_wait(s_bar + cur, (phase >> cur) & 1u);
-            phase ^= 1u << cur;
-            const B k0 = sb[0];
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                if (static_cast<std::uint32_t>(i * LC_BLOCK) >= len) break;  // rows past len stay unused
-                const std::uint32_t li = static_cast<std::uint32_t>(i * LC_BLOCK + tid);
-                const B v = li < len ? sb[li] : k0;  // padding repeats key 0 (neutral below)
-                orx |= v ^ k0;
-                k[i] = v ^ X;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) orx |= __shfl_xor_sync(FULL, orx, o);
-        if (lane == 0) red[warp] = orx;
-        const int nb_want = min(LC_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
-        const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
-        if (nwords_w >= 4) {
-            for (int i = tid; i < nwords_w / 4; i += LC_BLOCK)
-                reinterpret_cast<uint4*>(s_cw)[i] = make_uint4(0, 0, 0, 0);
-        } else if (tid < nwords_w) {
-            s_cw[tid] = 0;
-        }
-        fence_proxy_async_smem();  // generic accesses to the other buffer precede its next TMA write
-        __syncthreads();
-        if (tid == 0 && r + gridDim.x < nr) issue(r + gridDim.x, cur ^ 1);
-        if (!ok_range) {
-            if (e - b > static_cast<std::uint64_t>(CAP) && tid == 0) {  // left for the segment fallback
-                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
-                big[1 + slot] = r;
-            }
-            continue;
-        }
-        B vary = lane < LC_WARPS ? red[lane] : B(0);
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
-        vary = __shfl_sync(FULL, vary, 0);
-        if (vary == 0) {  // every key equal: the range is already sorted
-            if (copy_equal)
-                for (std::uint32_t j = tid; j < len; j += LC_BLOCK) out[b + j] = static_cast<T>(k[0] ^ X);
-            continue;
-        }
-        const int hb = 63 - __clzll(static_cast<long long>(vary));
-        const int nb = max(1, min(nb_want, hb + 1));
-        const int shift = hb + 1 - nb;
-        const std::uint32_t bmask = (1u << nb) - 1u;
-        const std::uint32_t nwords = 1u << (nb - 1);
-
-        // ---- counting: one shared atomic per key on its bin's half word -> slot in the bin ----
-        // slots (< LC_MAX_BIN = 48: 6 bits) packed five per word; bins are recomputed from the keys
-        constexpr int SW = (ITEMS + 4) / 5;
-        std::uint32_t sl[SW];
-#pragma unroll
-        for (int w = 0; w < SW; ++w) sl[w] = 0;
-        bool over = false;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            if (static_cast<std::uint32_t>(i * LC_BLOCK) >= len) break;
-            const bool ok = static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len;
-            const std::uint32_t bn = static_cast<std::uint32_t>(k[i] >> shift) & bmask;
-            const std::uint32_t sh = (bn & 1u) << 4;
-            const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
-            const std::uint32_t slot = (old >> sh) & 0xffffu;
-            over |= ok && slot >= LC_MAX_BIN;
-            sl[i / 5] |= (slot & 0x3fu) << (6 * (i % 5));
-        }
-        if (__syncthreads_or(over)) {  // clustered keys: the stable radix kernel takes the range
-            if (tid == 0) {
-                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(redo), 1ull);
-                redo[1 + slot] = r;
-            }
-            continue;
-        }
-        // ---- exclusive scan of the packed counts -> packed u16 bin starts (as local_count) ----
-        lc_scan_counts(s_cw, nwords, len, s_wsum);
-        __syncthreads();
-        // ---- keys into bin order (the range's own TMA buffer is free: keys are in registers) ----
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            if (static_cast<std::uint32_t>(i * LC_BLOCK) >= len) break;
-            if (static_cast<std::uint32_t>(i * LC_BLOCK + tid) < len)
-                sb[s_c16[static_cast<std::uint32_t>(k[i] >> shift) & bmask] + ((sl[i / 5] >> (6 * (i % 5))) & 0x3fu)] = k[i];
-        }
-        __syncthreads();
-        // ---- each position ranks its key inside its bin: final slot = bin start + #(key, pos) smaller ----
-        lc_rank_store<B>(sb, s_c16, len, B(0), shift, bmask, [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>(v ^ X); });
-    }  // ranges
-}
-
-// Big-range counting stage (n >= 2^29 after two MSD levels): ranges of up to LB_CAP = 18432
-// keys -- a whole 16-bit bucket of a 2^30-key sort -- in ONE CTA per SM (the key buffer takes
-// 144 KB of shared memory; 18 keys per thread of 1024 in registers), so two partition levels suffice
-// where the 4608-key stage needed a third level and its 24-bit histogram. The algorithm is
-// local_count3's (up to 2^15 packed u16 bins, one shared atomic per key, scan, bin-order
-// scatter, per-position rank; ranges = aligned groups of 1, 2, 4 or 8 16-bit buckets, so the
-// OR-reduced varying bits are exact -- a range cut at arbitrary bucket boundaries could
-// straddle an aligned boundary and crowd a few bins); the differences: the single buffer (the
-// next range's TMA copy is issued once this range's rank loop is done) and the scan over up
-// to 16384 counter words. A bin over LC_MAX_BIN keys sends the range to the segment fallback
-// (big list: the stable redo kernel holds only 6144 keys).
-#ifndef AKB_LB_BLOCK
-#define AKB_LB_BLOCK 1024
-#endif
-constexpr int LB_BLOCK = AKB_LB_BLOCK;
-constexpr int LB_WARPS = LB_BLOCK / 32;
-constexpr int LB_ITEMS = 18432 / LB_BLOCK;
-constexpr int LB_CAP = LB_BLOCK * LB_ITEMS;  // 18432 keys
-constexpr int LB_MAX_BITS = 15;
-constexpr int LB_WORDS = (1 << LB_MAX_BITS) / 2;  // 16384 counter words = 64 KB
-
-template <typename T>
-struct lb_smem {
-    static constexpr std::size_t buf_bytes = (sizeof(T) * (LB_CAP + 2) + 15) & ~std::size_t(15);
-    static constexpr std::size_t buf_off = 0;
-    static constexpr std::size_t cnt_off = buf_bytes;
-    static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LB_WORDS + 4);
-    static constexpr std::size_t red_off = cnt_off + cnt_bytes;                 // WARPS x u64 (+ spare)
-    static constexpr std::size_t wsum_off = red_off + 2 * LB_WARPS * sizeof(std::uint64_t);
-    static constexpr std::size_t bar_off = wsum_off + LB_WARPS * sizeof(std::uint32_t);
-    static constexpr std::size_t total = bar_off + sizeof(std::uint64_t);
-};
-
-// Exclusive scan of nwords (a power of two, <= LB_WORDS) packed u16 counts into packed u16
-// starts: warp w owns words [w * wpw, (w + 1) * wpw); within it, row q of 128 words is read
-// as one 16-byte quad per lane (conflict-free). Contains __syncthreads().
-__device__ __forceinline__ void lb_scan_counts(std::uint32_t* s_cw, std::uint32_t nwords, std::uint32_t len,
+// Exclusive scan of nwords (a power of two) packed u16 counts into packed u16 starts, any
+// table size (NT threads): warp w owns words [w * wpw, (w + 1) * wpw); within it, row q of
+// 128 words is read as one 16-byte quad per lane (conflict-free); more than two rows per
+// warp are scanned in two reads (totals, then starts). Contains __syncthreads().
+template <int NT>
+__device__ __forceinline__ void wide_scan_counts(std::uint32_t* s_cw, std::uint32_t nwords, std::uint32_t len,
                                                std::uint32_t* s_wsum) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const std::uint32_t wpw = nwords / LB_WARPS;
-    if (wpw < 128) {  // small tables: the single-CTA stage's scan
-        lc_scan_counts<LB_BLOCK>(s_cw, nwords, len, s_wsum);
+    const std::uint32_t wpw = nwords / (NT / 32);
+    if (wpw <= 2 * 128) {  // up to two quads per lane: held in registers by the one-read scan
+        lc_scan_counts<NT>(s_cw, nwords, len, s_wsum);
         return;
     }
-    const std::uint32_t nq = wpw / 128;  // 1 .. 8
+    const std::uint32_t nq = wpw / 128;
     std::uint32_t* wbase = s_cw + warp * wpw + 4 * lane;
     // pass 1: the warp's total; pass 2: per row, a warp scan of the quad sums (recomputed
     // rather than kept: registers hold the range's keys)
@@ -1692,6 +1524,182 @@ __device__ __forceinline__ void lb_scan_counts(std::uint32_t* s_cw, std::uint32_
     }
     if (tid == 0) reinterpret_cast<std::uint16_t*>(s_cw)[2 * nwords] = static_cast<std::uint16_t>(len);
 }
+
+template <typename T, int ITEMS, bool DESC, int NT = LC_BLOCK>
+__global__ void __launch_bounds__(NT, lc3_smem<T, ITEMS, NT>::MINB)
+    local_count3_kernel(const T* __restrict__ in, T* __restrict__ out, const std::uint64_t* __restrict__ cuts,
+                        std::uint64_t J, std::uint64_t* big, std::uint64_t* redo,
+                        const std::uint64_t* __restrict__ dplan) {
+    using L = lc3_smem<T, ITEMS, NT>;
+    constexpr int W = NT / 32;
+    using B = typename key_traits<T>::bits;
+    constexpr int CAP = L::CAP;
+    static_assert(sizeof(T) == 8, "8-byte keys");
+    constexpr B X = (std::is_signed_v<T> ? (B(1) << 63) : B(0)) ^ (DESC ? ~B(0) : B(0));  // raw <-> ordered
+    extern __shared__ __align__(16) unsigned char smem[];
+    B* s_red = reinterpret_cast<B*>(smem + L::red_off);  // [2][WARPS] OR partials
+    std::uint32_t* s_wsum = reinterpret_cast<std::uint32_t*>(smem + L::wsum_off);
+    std::uint64_t* s_bar = reinterpret_cast<std::uint64_t*>(smem + L::bar_off);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto fits = [&](std::uint64_t rb, std::uint64_t re) {
+        return re > rb && re - rb <= static_cast<std::uint64_t>(CAP);
+    };
+    auto issue = [&](std::uint64_t r, int q) {  // one thread
+        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
+        if (!fits(rb, re)) return;
+        const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
+        const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
+        mbar_arrive_expect_tx(s_bar + q, bytes);
+        bulk_g2s(smem + L::buf_off + q * L::buf_bytes, in + a0, bytes, s_bar + q);
+    };
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        mbar_init(s_bar + 1, 1);
+        mbar_init_fence();
+    }
+    __syncthreads();
+    // ranges < 2^32 (n / 256 at most); a device plan (dplan: {mode, group, J}) overrides J
+    const std::uint32_t nr = static_cast<std::uint32_t>(dplan ? (dplan[0] ? 0 : dplan[2]) : J);
+    if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x, 0);
+    std::uint32_t phase = 0;  // bit q = parity of buffer q's next completion
+    const bool copy_equal = in != out;
+
+#pragma unroll 1
+    for (std::uint32_t r = blockIdx.x, it = 0; r < nr; r += gridDim.x, ++it) {
+        const int cur = static_cast<int>(it & 1);
+        const std::uint64_t b = cuts[r], e = cuts[r + 1];
+        const bool ok_range = fits(b, e);
+        const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
+        B* sb = reinterpret_cast<B*>(smem + L::buf_off + cur * L::buf_bytes) + static_cast<std::uint32_t>(b & 1);
+        B* red = s_red + cur * W;
+        // packed u16 counts / starts, one table per parity of the range
+        std::uint32_t* s_cw = reinterpret_cast<std::uint32_t*>(smem + (cur ? L::cnt2_off : L::cnt_off));
+        const std::uint16_t* s_c16 = reinterpret_cast<const std::uint16_t*>(s_cw);
+        B k[ITEMS];
+        B orx = 0;
+        if (ok_range) {
+            mbar_wait(s_bar + cur, (phase >> cur) & 1u);
+            phase ^= 1u << cur;
+            const B k0 = sb[0];
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                if (static_cast<std::uint32_t>(i * NT) >= len) break;  // rows past len stay unused
+                const std::uint32_t li = static_cast<std::uint32_t>(i * NT + tid);
+                const B v = li < len ? sb[li] : k0;  // padding repeats key 0 (neutral below)
+                orx |= v ^ k0;
+                k[i] = v ^ X;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) orx |= __shfl_xor_sync(FULL, orx, o);
+        if (lane == 0) red[warp] = orx;
+        const int nb_want = min(LC_MAX_BITS, (len <= 1 ? 0 : 32 - __clz(len - 1)) + AKB_LC_EXTRA);
+        const int nwords_w = nb_want >= 1 ? (1 << (nb_want - 1)) : 1;
+        if (nwords_w >= 4) {
+            for (int i = tid; i < nwords_w / 4; i += NT)
+                reinterpret_cast<uint4*>(s_cw)[i] = make_uint4(0, 0, 0, 0);
+        } else if (tid < nwords_w) {
+            s_cw[tid] = 0;
+        }
+        fence_proxy_async_smem();  // generic accesses to the other buffer precede its next TMA write
+        __syncthreads();
+        if (tid == 0 && r + gridDim.x < nr) issue(r + gridDim.x, cur ^ 1);
+        if (!ok_range) {
+            if (e - b > static_cast<std::uint64_t>(CAP) && tid == 0) {  // left for the segment fallback
+                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
+                big[1 + slot] = r;
+            }
+            continue;
+        }
+        B vary = lane < W ? red[lane] : B(0);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) vary |= __shfl_xor_sync(FULL, vary, o);
+        vary = __shfl_sync(FULL, vary, 0);
+        if (vary == 0) {  // every key equal: the range is already sorted
+            if (copy_equal)
+                for (std::uint32_t j = tid; j < len; j += NT) out[b + j] = static_cast<T>(k[0] ^ X);
+            continue;
+        }
+        const int hb = 63 - __clzll(static_cast<long long>(vary));
+        const int nb = max(1, min(nb_want, hb + 1));
+        const int shift = hb + 1 - nb;
+        const std::uint32_t bmask = (1u << nb) - 1u;
+        const std::uint32_t nwords = 1u << (nb - 1);
+
+        // ---- counting: one shared atomic per key on its bin's half word -> slot in the bin ----
+        // slots (< LC_MAX_BIN = 48: 6 bits) packed five per word; bins are recomputed from the keys
+        constexpr int SW = (ITEMS + 4) / 5;
+        std::uint32_t sl[SW];
+#pragma unroll
+        for (int w = 0; w < SW; ++w) sl[w] = 0;
+        bool over = false;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            if (static_cast<std::uint32_t>(i * NT) >= len) break;
+            const bool ok = static_cast<std::uint32_t>(i * NT + tid) < len;
+            const std::uint32_t bn = static_cast<std::uint32_t>(k[i] >> shift) & bmask;
+            const std::uint32_t sh = (bn & 1u) << 4;
+            const std::uint32_t old = atom_add_shared_if(ok, s_cw + (bn >> 1), 1u << sh);
+            const std::uint32_t slot = (old >> sh) & 0xffffu;
+            over |= ok && slot >= LC_MAX_BIN;
+            sl[i / 5] |= (slot & 0x3fu) << (6 * (i % 5));
+        }
+        if (__syncthreads_or(over)) {  // clustered keys: the stable radix kernel takes the range
+            if (tid == 0) {
+                const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(redo), 1ull);
+                redo[1 + slot] = r;
+            }
+            continue;
+        }
+        // ---- exclusive scan of the packed counts -> packed u16 bin starts (as local_count) ----
+        wide_scan_counts<NT>(s_cw, nwords, len, s_wsum);
+        __syncthreads();
+        // ---- keys into bin order (the range's own TMA buffer is free: keys are in registers) ----
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            if (static_cast<std::uint32_t>(i * NT) >= len) break;
+            if (static_cast<std::uint32_t>(i * NT + tid) < len)
+                sb[s_c16[static_cast<std::uint32_t>(k[i] >> shift) & bmask] + ((sl[i / 5] >> (6 * (i % 5))) & 0x3fu)] = k[i];
+        }
+        __syncthreads();
+        // ---- each position ranks its key inside its bin: final slot = bin start + #(key, pos) smaller ----
+        lc_rank_store<B, NT>(sb, s_c16, len, B(0), shift, bmask, [&](std::uint32_t rk, B v) { out[b + rk] = static_cast<T>(v ^ X); });
+    }  // ranges
+}
+
+// Big-range counting stage (n >= 2^29 after two MSD levels): ranges of up to LB_CAP = 18432
+// keys -- a whole 16-bit bucket of a 2^30-key sort -- in ONE CTA per SM (the key buffer takes
+// 144 KB of shared memory; 18 keys per thread of 1024 in registers), so two partition levels suffice
+// where the 4608-key stage needed a third level and its 24-bit histogram. The algorithm is
+// local_count3's (up to 2^15 packed u16 bins, one shared atomic per key, scan, bin-order
+// scatter, per-position rank; ranges = aligned groups of 1, 2, 4 or 8 16-bit buckets, so the
+// OR-reduced varying bits are exact -- a range cut at arbitrary bucket boundaries could
+// straddle an aligned boundary and crowd a few bins); the differences: the single buffer (the
+// next range's TMA copy is issued once this range's rank loop is done) and the scan over up
+// to 16384 counter words. A bin over LC_MAX_BIN keys sends the range to the segment fallback
+// (big list: the stable redo kernel holds only 6144 keys).
+#ifndef AKB_LB_BLOCK
+#define AKB_LB_BLOCK 1024
+#endif
+constexpr int LB_BLOCK = AKB_LB_BLOCK;
+constexpr int LB_WARPS = LB_BLOCK / 32;
+constexpr int LB_ITEMS = 18432 / LB_BLOCK;
+constexpr int LB_CAP = LB_BLOCK * LB_ITEMS;  // 18432 keys
+constexpr int LB_MAX_BITS = 15;
+constexpr int LB_WORDS = (1 << LB_MAX_BITS) / 2;  // 16384 counter words = 64 KB
+
+template <typename T>
+struct lb_smem {
+    static constexpr std::size_t buf_bytes = (sizeof(T) * (LB_CAP + 2) + 15) & ~std::size_t(15);
+    static constexpr std::size_t buf_off = 0;
+    static constexpr std::size_t cnt_off = buf_bytes;
+    static constexpr std::size_t cnt_bytes = sizeof(std::uint32_t) * (LB_WORDS + 4);
+    static constexpr std::size_t red_off = cnt_off + cnt_bytes;                 // WARPS x u64 (+ spare)
+    static constexpr std::size_t wsum_off = red_off + 2 * LB_WARPS * sizeof(std::uint64_t);
+    static constexpr std::size_t bar_off = wsum_off + LB_WARPS * sizeof(std::uint32_t);
+    static constexpr std::size_t total = bar_off + sizeof(std::uint64_t);
+};
+
 
 template <typename T, bool DESC>
 __global__ void __launch_bounds__(LB_BLOCK, 1)
@@ -1807,7 +1815,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
                     big[1 + slot] = r;
                 }
             } else {
-                lb_scan_counts(s_cw, nwords, len, s_wsum);
+                wide_scan_counts<LB_BLOCK>(s_cw, nwords, len, s_wsum);
                 __syncthreads();
 #pragma unroll
                 for (int i = 0; i < ITEMS; ++i) {
@@ -2124,12 +2132,15 @@ void launch_local_count(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cut
     const int tok = ctx_prof_begin(c, KF_LOCAL);
     const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * CS::MINB));
     if ((reinterpret_cast<std::uintptr_t>(G) & 15) == 0) {  // TMA-fed lean kernel
-        using C3 = lc3_smem<T, CITEMS>;
+        constexpr int NT3 = LC3_BLOCK;
+        constexpr int CITEMS3 = ITEMS * LOCAL_BLOCK / NT3;
+        static_assert(CITEMS3 * NT3 == ITEMS * LOCAL_BLOCK, "same range capacity");
+        using C3 = lc3_smem<T, CITEMS3, NT3>;
         const unsigned grid3 =
             static_cast<unsigned>(std::min<std::uint64_t>(J, static_cast<std::uint64_t>(c->sm_count) * C3::MINB));
-        auto kern = desc ? local_count3_kernel<T, CITEMS, true> : local_count3_kernel<T, CITEMS, false>;
+        auto kern = desc ? local_count3_kernel<T, CITEMS3, true, NT3> : local_count3_kernel<T, CITEMS3, false, NT3>;
         smem_attr(c, kern, C3::total);
-        kern<<<grid3, LC_BLOCK, C3::total, c->stream>>>(G, kout, cuts, J, big, redo, dplan);
+        kern<<<grid3, NT3, C3::total, c->stream>>>(G, kout, cuts, J, big, redo, dplan);
     } else {
         auto kern = desc ? local_count_kernel<T, CITEMS, true> : local_count_kernel<T, CITEMS, false>;
         smem_attr(c, kern, CS::total);
