@@ -1739,8 +1739,19 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
     const bool copy_equal = in != out;
 
 #pragma unroll 1
+    // the range bounds are loaded one range ahead (one CTA per SM: a cold global load per
+    // range would sit on the critical path)
+    std::uint64_t nb_ = 0, ne_ = 0;
+    if (blockIdx.x < nr) {
+        nb_ = cuts[blockIdx.x];
+        ne_ = cuts[blockIdx.x + 1];
+    }
     for (std::uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
-        const std::uint64_t b = cuts[r], e = cuts[r + 1];
+        const std::uint64_t b = nb_, e = ne_;
+        if (r + gridDim.x < nr) {
+            nb_ = cuts[r + gridDim.x];
+            ne_ = cuts[r + gridDim.x + 1];
+        }
         const bool ok_range = fits(b, e);
         const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
         B* sb = reinterpret_cast<B*>(smem + L::buf_off) + static_cast<std::uint32_t>(b & 1);
