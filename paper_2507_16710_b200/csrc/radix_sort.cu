@@ -1564,10 +1564,19 @@ __global__ void __launch_bounds__(NT, lc3_smem<T, ITEMS, NT>::MINB)
     std::uint32_t phase = 0;  // bit q = parity of buffer q's next completion
     const bool copy_equal = in != out;
 
+    std::uint64_t nb_ = 0, ne_ = 0;  // the range bounds, loaded one range ahead
+    if (blockIdx.x < nr) {
+        nb_ = cuts[blockIdx.x];
+        ne_ = cuts[blockIdx.x + 1];
+    }
 #pragma unroll 1
     for (std::uint32_t r = blockIdx.x, it = 0; r < nr; r += gridDim.x, ++it) {
         const int cur = static_cast<int>(it & 1);
-        const std::uint64_t b = cuts[r], e = cuts[r + 1];
+        const std::uint64_t b = nb_, e = ne_;
+        if (r + gridDim.x < nr) {
+            nb_ = cuts[r + gridDim.x];
+            ne_ = cuts[r + gridDim.x + 1];
+        }
         const bool ok_range = fits(b, e);
         const std::uint32_t len = ok_range ? static_cast<std::uint32_t>(e - b) : 0u;
         B* sb = reinterpret_cast<B*>(smem + L::buf_off + cur * L::buf_bytes) + static_cast<std::uint32_t>(b & 1);
