@@ -1544,14 +1544,14 @@ __global__ void __launch_bounds__(NT, lc3_smem<T, ITEMS, NT>::MINB)
     auto fits = [&](std::uint64_t rb, std::uint64_t re) {
         return re > rb && re - rb <= static_cast<std::uint64_t>(CAP);
     };
-    auto issue = [&](std::uint64_t r, int q) {  // one thread
-        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
+    auto issue_at = [&](std::uint64_t rb, std::uint64_t re, int q) {  // one thread
         if (!fits(rb, re)) return;
         const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
         const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
         mbar_arrive_expect_tx(s_bar + q, bytes);
         bulk_g2s(smem + L::buf_off + q * L::buf_bytes, in + a0, bytes, s_bar + q);
     };
+    auto issue = [&](std::uint64_t r, int q) { issue_at(cuts[r], cuts[r + 1], q); };
     if (tid == 0) {
         mbar_init(s_bar, 1);
         mbar_init(s_bar + 1, 1);
@@ -1612,7 +1612,7 @@ __global__ void __launch_bounds__(NT, lc3_smem<T, ITEMS, NT>::MINB)
         }
         fence_proxy_async_smem();  // generic accesses to the other buffer precede its next TMA write
         __syncthreads();
-        if (tid == 0 && r + gridDim.x < nr) issue(r + gridDim.x, cur ^ 1);
+        if (tid == 0 && r + gridDim.x < nr) issue_at(nb_, ne_, cur ^ 1);  // the bounds loaded ahead
         if (!ok_range) {
             if (e - b > static_cast<std::uint64_t>(CAP) && tid == 0) {  // left for the segment fallback
                 const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(big), 1ull);
@@ -1729,8 +1729,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
     auto fits = [&](std::uint64_t rb, std::uint64_t re) {
         return re > rb && re - rb <= static_cast<std::uint64_t>(LB_CAP);
     };
-    auto issue = [&](std::uint32_t r) {  // one thread; the buffer is idle
-        const std::uint64_t rb = cuts[r], re = cuts[r + 1];
+    auto issue_at = [&](std::uint64_t rb, std::uint64_t re) {  // one thread; the buffer is idle
         if (!fits(rb, re)) return;
         const std::uint64_t a0 = rb & ~std::uint64_t(1), a1 = (re + 1) & ~std::uint64_t(1);
         const std::uint32_t bytes = static_cast<std::uint32_t>((a1 - a0) * sizeof(T));
@@ -1743,7 +1742,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
     }
     __syncthreads();
     const std::uint32_t nr = static_cast<std::uint32_t>(dplan ? (dplan[0] ? 0 : dplan[2]) : J);
-    if (tid == 0 && blockIdx.x < nr) issue(blockIdx.x);
+    if (tid == 0 && blockIdx.x < nr) issue_at(cuts[blockIdx.x], cuts[blockIdx.x + 1]);
     std::uint32_t phase = 0;
     const bool copy_equal = in != out;
 
@@ -1852,7 +1851,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
         // the buffer and the counters are idle once every thread is here: next range's copy
         fence_proxy_async_smem();
         __syncthreads();
-        if (tid == 0 && r + gridDim.x < nr) issue(r + gridDim.x);
+        if (tid == 0 && r + gridDim.x < nr) issue_at(nb_, ne_);  // the bounds loaded ahead
     }  // ranges
 }
 
