@@ -244,35 +244,8 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
     const std::uint64_t t0 = static_cast<std::uint64_t>(blockIdx.x) * MP_TILE;
     const std::uint32_t len = static_cast<std::uint32_t>(n - t0 < MP_TILE ? n - t0 : MP_TILE);
 
-    // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL L > 1 = the 8L-bit prefixes
-    // of the (already 8(L-1)-bit partitioned) tile, relative to its first key's 8(L-1)-bit
-    // prefix (cursor index = the 8L-bit prefix)
-    if (plan != nullptr && plan[0] != 0) return;  // device plan: not applicable, nothing written
-    using G = mp_level<LEVEL>;
-    constexpr int DB = G::DB;
-    const int TOP = LEVEL == 0 ? plan[1] : G::TOP;  // shift of the digit (cursor index = key >> TOP)
-    constexpr std::uint32_t DMASK = LEVEL == 0 ? 0xffu : 0xffffffffu;
-    std::uint32_t lo16 = 0, span = 1;
-    if constexpr (G::PB > 0) {
-        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> (TOP + DB));
-        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> (TOP + DB));
-        lo16 = f << DB;
-        span = l - f + 1;
-    }
-    const std::uint32_t nbins = span << DB;
-    if (G::PB > 0 && span > MP_SPAN) {
-        // tiny buckets (skewed keys): per-key cursor claims, written straight out
-        for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
-            const T k = in[t0 + j];
-            const std::uint32_t bp = static_cast<std::uint32_t>(ord64(k, dsc) >> TOP);
-            const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + bp), 1ull);
-            out[p] = k;
-        }
-        return;
-    }
-    for (std::uint32_t i = tid; i < nbins * MP_PARTS; i += MP_BLOCK) s_cnt[i] = 0;
-
-    // load: 128-bit vectors when the tile is full and aligned
+    // load first: 128-bit vectors when the tile is full and aligned; the plan / span reads
+    // below are then in flight together with the tile instead of ahead of it
     T k[MP_ITEMS];
     const bool vec = len == MP_TILE && (reinterpret_cast<std::uintptr_t>(in + t0) & 15) == 0;
     if (vec) {
@@ -292,6 +265,35 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
                 k[2 * i + h] = li < len ? in[t0 + li] : T(0);
             }
     }
+
+    // bin range of this tile: LEVEL 1 = the 256 top digits; LEVEL L > 1 = the 8L-bit prefixes
+    // of the (already 8(L-1)-bit partitioned) tile, relative to its first key's 8(L-1)-bit
+    // prefix (cursor index = the 8L-bit prefix)
+    if (plan != nullptr && plan[0] != 0) return;  // device plan: not applicable, nothing written
+    using G = mp_level<LEVEL>;
+    constexpr int DB = G::DB;
+    const int TOP = LEVEL == 0 ? plan[1] : G::TOP;  // shift of the digit (cursor index = key >> TOP)
+    constexpr std::uint32_t DMASK = LEVEL == 0 ? 0xffu : 0xffffffffu;
+    std::uint32_t lo16 = 0, span = 1;
+    if constexpr (G::PB > 0) {
+        const std::uint32_t f = static_cast<std::uint32_t>(ord64(in[t0], dsc) >> (TOP + DB));
+        const std::uint32_t l = static_cast<std::uint32_t>(ord64(in[t0 + len - 1], dsc) >> (TOP + DB));
+        lo16 = f << DB;
+        span = l - f + 1;
+    }
+    const std::uint32_t nbins = span << DB;
+    if (G::PB > 0 && span > MP_SPAN) {
+        // tiny buckets (skewed keys): per-key cursor claims, written straight out
+        for (std::uint32_t j = tid; j < len; j += MP_BLOCK) {
+            const T key = in[t0 + j];
+            const std::uint32_t bp = static_cast<std::uint32_t>(ord64(key, dsc) >> TOP);
+            const unsigned long long p = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + bp), 1ull);
+            out[p] = key;
+        }
+        return;
+    }
+    for (std::uint32_t i = tid; i < nbins * MP_PARTS; i += MP_BLOCK) s_cnt[i] = 0;
+
     auto item_ok = [&](int i) { return 2 * ((i / 2) * MP_BLOCK + tid) + (i & 1) < static_cast<int>(len); };
     auto bin_of = [&](T key) {
         const std::uint64_t o = ord64(key, dsc);
