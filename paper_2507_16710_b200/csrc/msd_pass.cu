@@ -324,6 +324,22 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
             c[q] = (static_cast<std::uint32_t>(q) < bpt * MP_PARTS && fs + q < nsub) ? s_cnt[fs + q] : 0u;
             sum += c[q];
         }
+        // global position of staged slot j in bin b = gofs[b] + j. The cursor claims are issued
+        // as soon as the counts are read and consumed only after the keys are staged: the
+        // global atomic round trip overlaps the scan, the start rewrite and the staging stores
+        std::uint64_t gclaim[BPTMAX];
+        std::uint32_t tot[BPTMAX];
+#pragma unroll
+        for (int bi = 0; bi < BPTMAX; ++bi) {
+            const std::uint32_t bin = fs / MP_PARTS + bi;
+            tot[bi] = 0;
+#pragma unroll
+            for (int q = 0; q < MP_PARTS; ++q) tot[bi] += c[bi * MP_PARTS + q];
+            gclaim[bi] = 0;
+            if (static_cast<std::uint32_t>(bi) < bpt && bin < nbins && tot[bi])
+                gclaim[bi] = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + bin),
+                                       static_cast<unsigned long long>(tot[bi]));
+        }
         std::uint32_t inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -336,28 +352,17 @@ __global__ void __launch_bounds__(MP_BLOCK, AKB_MP_MINB)
 #pragma unroll
         for (int w = 0; w < MP_BLOCK / 32; ++w) wp += w < warp ? s_wsum[w] : 0u;
         std::uint32_t run = wp + inc - sum;
-        // global position of staged slot j in bin b = gofs[b] + j. The cursor claims are issued
-        // here and their results consumed only after the keys are staged: the global atomic
-        // round trip overlaps the rewrite of the starts and the staging stores
-        std::uint32_t r2 = run;
-        std::uint64_t gclaim[BPTMAX];
         std::uint32_t gbase[BPTMAX];
+        {
+            std::uint32_t r2 = run;
 #pragma unroll
-        for (int bi = 0; bi < BPTMAX; ++bi) {
-            const std::uint32_t bin = fs / MP_PARTS + bi;
-            std::uint32_t tot = 0;
-#pragma unroll
-            for (int q = 0; q < MP_PARTS; ++q) tot += c[bi * MP_PARTS + q];
-            gclaim[bi] = 0;
-            gbase[bi] = r2;
-            if (static_cast<std::uint32_t>(bi) < bpt && bin < nbins && tot)
-                gclaim[bi] = atomicAdd(reinterpret_cast<unsigned long long*>(cursors + lo16 + bin),
-                                       static_cast<unsigned long long>(tot));
-            else
-                gbase[bi] = 0xffffffffu;  // no claim for this bin
-            r2 += tot;
+            for (int bi = 0; bi < BPTMAX; ++bi) {
+                const std::uint32_t bin = fs / MP_PARTS + bi;
+                gbase[bi] = (static_cast<std::uint32_t>(bi) < bpt && bin < nbins && tot[bi]) ? r2 : 0xffffffffu;
+                r2 += tot[bi];
+            }
         }
-        __syncthreads();  // every count read before the starts overwrite them
+        // (each thread rewrites only the counters it read: no barrier before the rewrite)
 #pragma unroll
         for (int q = 0; q < MAXC; ++q)
             if (static_cast<std::uint32_t>(q) < bpt * MP_PARTS && fs + q < nsub) {
