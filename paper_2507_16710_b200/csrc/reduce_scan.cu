@@ -3,6 +3,7 @@
 #include <type_traits>
 
 #include "reduce_scan.cuh"
+#include "tma.cuh"
 
 namespace akb {
 
@@ -356,7 +357,14 @@ __global__ void __launch_bounds__(scan_cfg<T>::BLOCK, 6)
     __shared__ A s_excl;
     __shared__ std::uint32_t s_tile_id;
     const int tid = threadIdx.x;
-    if (tid == 0) s_tile_id = atomicAdd(tile_counter, 1u);
+    if (tid == 0) {
+        // the tile id comes from the ticket below (look-back order); tickets follow the launch
+        // order closely, so the tile this CTA's index names -- read by this or a neighbouring
+        // CTA -- is fetched into L2 while the ticket round trip is in flight
+        const std::uint64_t pb = static_cast<std::uint64_t>(blockIdx.x) * TILE;
+        if (VECIO && pb + TILE <= n) bulk_prefetch_l2(x + pb, static_cast<std::uint32_t>(TILE * sizeof(T)));
+        s_tile_id = atomicAdd(tile_counter, 1u);
+    }
     __syncthreads();
     const std::uint32_t tile = s_tile_id;
     const std::uint64_t base = static_cast<std::uint64_t>(tile) * TILE;

@@ -27,6 +27,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// L2 prefetch of [src, src + bytes) by the TMA engine (16-byte aligned, bytes a multiple of 16);
+// no completion to wait for.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, std::uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
     asm volatile(
         "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
