@@ -314,7 +314,19 @@ __global__ void __launch_bounds__(tile_cfg<T, V, MODE>::BLOCK, tile_cfg<T, V, MO
     const int vw = HALF ? warp * 2 + (lane >> 4) : warp;
     const int gl = HALF ? (lane & 15) : lane;
     const bool dsc = desc != 0;
-    if (tid == 0) s_misc[0] = atomicAdd(tile_counter, 1u);
+    if (tid == 0) {
+        // tile ids come from the ticket (look-back order) and follow the launch order closely:
+        // the tile this CTA's index names is fetched into L2 while the ticket is in flight
+        const std::uint64_t pb = static_cast<std::uint64_t>(blockIdx.x) * TILE;
+        if (MODE != SORT_LOWMEM && pb + TILE <= n) {
+            if ((reinterpret_cast<std::uintptr_t>(kin + pb) & 15) == 0 && (TILE * sizeof(T)) % 16 == 0)
+                bulk_prefetch_l2(kin + pb, static_cast<std::uint32_t>(TILE * sizeof(T)));
+            if (MODE == SORT_PAIRS || (MODE == SORT_IOTA && pass_index != 0))
+                if ((reinterpret_cast<std::uintptr_t>(vin + pb) & 15) == 0 && (TILE * sizeof(V)) % 16 == 0)
+                    bulk_prefetch_l2(vin + pb, static_cast<std::uint32_t>(TILE * sizeof(V)));
+        }
+        s_misc[0] = atomicAdd(tile_counter, 1u);
+    }
     for (int i = tid; i < VW * RADIX; i += BLOCK) s_whist[i] = 0;
     if constexpr (HW_MATCH == MATCH_SMEM || HW_MATCH == MATCH_HYBRID) {
         std::uint32_t* s_match = reinterpret_cast<std::uint32_t*>(smem + L::match_off);
