@@ -1057,6 +1057,9 @@ constexpr int LC3_BLOCK = AKB_LC3_BLOCK;
 constexpr int LC_MAX_BITS = 13;                        // up to 8192 bins (u16 counts, 2 per word)
 constexpr int LC_WORDS = (1 << LC_MAX_BITS) / 2;       // 4096 counter words = 16 KB
 constexpr std::uint32_t LC_MAX_BIN = 48;
+#ifndef AKB_RANK_BRANCHFREE
+#define AKB_RANK_BRANCHFREE 1
+#endif
 #ifndef AKB_RANK_UNROLL
 #define AKB_RANK_UNROLL 6  // positions of local_count3's rank loop in flight per thread (r02: 3 -> 6, -1.6%)
 #endif
@@ -1475,12 +1478,24 @@ __device__ __forceinline__ void lc_rank_store(const B* sb, const std::uint16_t* 
         const B v = sb[x];
         const std::uint32_t bn = static_cast<std::uint32_t>((v - kmin) >> shift) & bmask;
         const std::uint32_t st = s_c16[bn], cnt = s_c16[bn + 1] - st;
+#if AKB_RANK_BRANCHFREE
+        // the first two members are compared without a branch: for a one-key bin st == x (the
+        // self-compare counts 0) and slot st + 1 is the next bin's first key or a spare slot of
+        // the buffer, masked out; lanes of a warp read near-consecutive slots
+        const B a0 = sb[st], a1 = sb[st + 1];
+        std::uint32_t rk = st + lex_less96(a0, st, v, x) + (cnt > 1 ? lex_less96(a1, st + 1, v, x) : 0u);
+        if (cnt > 2) {
+#pragma unroll 1
+            for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(sb[y], y, v, x);
+        }
+#else
         std::uint32_t rk = x;
         if (cnt > 1) {
             rk = st + lex_less96(sb[st], st, v, x) + lex_less96(sb[st + 1], st + 1, v, x);
 #pragma unroll 1
             for (std::uint32_t y = st + 2; y < st + cnt; ++y) rk += lex_less96(sb[y], y, v, x);
         }
+#endif
         store(rk, v);
     }
 }
