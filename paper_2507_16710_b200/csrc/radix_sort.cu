@@ -38,8 +38,14 @@ constexpr std::uint32_t FULL = 0xffffffffu;
 #ifndef AKB_OS_ITEMS
 #define AKB_OS_ITEMS 16  // keys per thread of a keys-only pass tile
 #endif
+// 4 + 4-byte (key, payload) pass tiles: 256 threads x 28 pairs (7168), 2 CTAs/SM, 128
+// registers. r02 sweep, sortperm 1e8 f32: 384 x 16 2.52 ms, 256 x 24 2.43, 256 x 28 2.36,
+// 256 x 32 2.36 (56 B of spills), 512 x 12 2.71, 256 x 16 (3 CTAs/SM) 2.57
 #ifndef AKB_OS_PAIR_ITEMS
-#define AKB_OS_PAIR_ITEMS 16  // elements per thread of a 4 + 4-byte (key, payload) pass tile
+#define AKB_OS_PAIR_ITEMS 28
+#endif
+#ifndef AKB_OS_PAIR_BLOCK
+#define AKB_OS_PAIR_BLOCK 256
 #endif
 #ifndef AKB_OS_BLOCK
 #define AKB_OS_BLOCK 384  // threads per pass CTA (>= RADIX)
@@ -77,8 +83,9 @@ __device__ std::uint64_t* g_phase = nullptr;
 
 template <typename T, typename V, int MODE>
 struct tile_cfg {
-    static constexpr int BLOCK = AKB_OS_BLOCK;
     static constexpr bool HAS_VALS = MODE != SORT_KEYS;
+    static constexpr bool PAIR8 = HAS_VALS && sizeof(T) + sizeof(V) <= 8;  // 4-byte key + 4-byte payload
+    static constexpr int BLOCK = PAIR8 ? AKB_OS_PAIR_BLOCK : AKB_OS_BLOCK;
     static constexpr int ITEMS =
         !HAS_VALS ? AKB_OS_ITEMS : (sizeof(T) + sizeof(V) <= 8 ? AKB_OS_PAIR_ITEMS : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
     static constexpr int TILE = BLOCK * ITEMS;
