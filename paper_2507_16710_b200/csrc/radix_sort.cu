@@ -41,6 +41,21 @@ constexpr std::uint32_t FULL = 0xffffffffu;
 // 4 + 4-byte (key, payload) pass tiles: 256 threads x 28 pairs (7168), 2 CTAs/SM, 128
 // registers. r02 sweep, sortperm 1e8 f32: 384 x 16 2.52 ms, 256 x 24 2.43, 256 x 28 2.36,
 // 256 x 32 2.36 (56 B of spills), 512 x 12 2.71, 256 x 16 (3 CTAs/SM) 2.57
+// Keys-only pass tiles (r02 sweeps, 2^27 keys): 4-byte keys 256 threads x 40 keys (f32 sort
+// onesweep 2.75 -> 2.26 ms; 384 x 16 before, 256 x 32 2.33, 256 x 48 2.26 with spills);
+// 8-byte keys 256 x 32 (f64 merge_sort 6.97 -> 6.25 ms; 256 x 24 6.52, 256 x 28 6.35)
+#ifndef AKB_OS_KEY4_ITEMS
+#define AKB_OS_KEY4_ITEMS 40
+#endif
+#ifndef AKB_OS_KEY4_BLOCK
+#define AKB_OS_KEY4_BLOCK 256
+#endif
+#ifndef AKB_OS_KEY8_ITEMS
+#define AKB_OS_KEY8_ITEMS 32
+#endif
+#ifndef AKB_OS_KEY8_BLOCK
+#define AKB_OS_KEY8_BLOCK 256
+#endif
 #ifndef AKB_OS_PAIR_ITEMS
 #define AKB_OS_PAIR_ITEMS 28
 #endif
@@ -85,9 +100,13 @@ template <typename T, typename V, int MODE>
 struct tile_cfg {
     static constexpr bool HAS_VALS = MODE != SORT_KEYS;
     static constexpr bool PAIR8 = HAS_VALS && sizeof(T) + sizeof(V) <= 8;  // 4-byte key + 4-byte payload
-    static constexpr int BLOCK = PAIR8 ? AKB_OS_PAIR_BLOCK : AKB_OS_BLOCK;
+    static constexpr bool KEY4 = !HAS_VALS && sizeof(T) <= 4;              // keys-only, 4-byte keys
+    static constexpr bool KEY8 = !HAS_VALS && sizeof(T) == 8;              // keys-only, 8-byte keys
+    static constexpr int BLOCK =
+        PAIR8 ? AKB_OS_PAIR_BLOCK : (KEY4 ? AKB_OS_KEY4_BLOCK : (KEY8 ? AKB_OS_KEY8_BLOCK : AKB_OS_BLOCK));
     static constexpr int ITEMS =
-        !HAS_VALS ? AKB_OS_ITEMS : (sizeof(T) + sizeof(V) <= 8 ? AKB_OS_PAIR_ITEMS : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
+        !HAS_VALS ? (KEY4 ? AKB_OS_KEY4_ITEMS : (KEY8 ? AKB_OS_KEY8_ITEMS : AKB_OS_ITEMS))
+                  : (sizeof(T) + sizeof(V) <= 8 ? AKB_OS_PAIR_ITEMS : (sizeof(T) + sizeof(V) <= 12 ? 12 : 10));
     static constexpr int TILE = BLOCK * ITEMS;
     static constexpr int MIN_BLOCKS = AKB_OS_MINB;
 };
