@@ -1,18 +1,22 @@
-// radix_sort.cu -- onesweep radix sort kernels (see radix_sort.cuh).
+// radix_sort.cu -- the sort kernels (see radix_sort.cuh).
 //
-// Pass kernel structure (one CTA per tile, tiles claimed in launch order):
-//   1. load the tile (warp-striped, coalesced) and extract 8-bit digits once
-//      (packed 4 per register);
-//   2. EARLY COUNTS: block digit histogram with shared atomics, published to the
-//      look-back chain immediately (AGG, or INC for tile 0), so successors see
-//      this tile's counts before it has ranked anything;
-//   3. stable warp ranking: hardware match.any (or 8 ballots) per item, leader
-//      bumps the warp's digit counter;
-//   4. warp-exclusive offsets + block scan of digit totals -> digit-ordered
-//      staging of keys (and payload) in shared memory;
-//   5. windowed decoupled look-back (4 predecessors in flight per digit) ->
-//      INC publish and global digit bases;
-//   6. scatter contiguous per-digit runs.
+// 1. Stable onesweep LSD pass (every payload mode, float keys, small / skewed inputs). Per
+//    tile: thread 0 prefetches the launch-order tile into L2 and takes a ticket (tiles are
+//    claimed in launch order, so a tile's predecessors are resident); keys (and payload) load
+//    warp-striped and their 8-bit digits are packed 4 per register; stable half-warp ranking
+//    (count and peer mask in one shared word per digit); the tile's digit counts are
+//    published to the decoupled look-back chain after ranking; digit-ordered staging in shared
+//    memory (a 4 + 4-byte (key, payload) pair as one 8-byte slot); windowed look-back (4
+//    predecessors per round trip); contiguous per-digit runs written out. Tile shapes per
+//    (key, payload) size: the AKB_OS_* knobs below.
+// 2. Keys-only 64-bit integers (hybrid_sort_keys): a device-planned two-level unstable MSD
+//    partition (msd_pass.cu), then a counting stage sorts every bucket range on chip --
+//    local_count3_kernel (ranges <= 4608 keys, 2 CTAs per SM, TMA double-buffered) or
+//    local_big_kernel (<= 18432 keys, one CTA per SM, n ~2^29..2^30); the rare clustered
+//    range falls back to the stable on-chip radix (local_redo_kernel), oversized ranges to a
+//    segment LSD. Small sorts (n <= 2^21) run a device-planned one-pass variant as a CUDA graph.
+// 3. merge_runs_counting: SIHSort's P-way merge of 64-bit integer runs by value tiles sorted
+//    with the counting stage.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>

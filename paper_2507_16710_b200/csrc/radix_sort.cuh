@@ -1,18 +1,14 @@
-// radix_sort.cuh -- stable onesweep LSD radix sort for sm_100a.
+// radix_sort.cuh -- the radix sort family for sm_100a.
 //
-// Replaces the reference's bottom-up merge sort (sort.hpp:123-170): both are
-// stable, so for every (keys, payload) input the output is identical.
-//
-// Per sort: one upfront pass computes all D digit histograms (D = key bits / 8),
-// then D onesweep passes each read the keys once and write them once:
-//   * tiles are claimed in launch order through an atomic tile counter, so a
-//     tile's predecessors are always resident (forward progress),
-//   * each warp ranks its keys with ballot-based match + per-warp smem digit
-//     counters (stable: order = warp, item, lane = input order),
-//   * tile digit counts are published to a decoupled look-back chain (one
-//     64-bit self-contained word per (tile, digit), epoch tagged),
-//   * keys are staged in shared memory in digit order and written out as
-//     contiguous per-digit runs (coalesced segments).
+// Replaces the reference's bottom-up merge sort (sort.hpp:123-170). The stable path (payload
+// modes, float keys): one upfront pass computes all D digit histograms (D = key bits / 8),
+// then D onesweep passes each read the keys once and write them once -- tiles claimed in
+// launch order through an atomic ticket (forward progress), stable half-warp ranking, tile
+// digit counts on a decoupled look-back chain (one 64-bit epoch-tagged word per (tile,
+// digit)), digit-ordered staging and contiguous per-digit runs. Keys-only 64-bit integers
+// take the hybrid (two unstable MSD partition passes + an on-chip counting stage per bucket
+// range): equal integer keys are identical bit patterns, so the result equals the stable
+// sort's.
 #pragma once
 
 #include <cstdint>
