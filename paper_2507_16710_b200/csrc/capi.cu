@@ -770,6 +770,7 @@ int ak_memcpy(ak_ctx* c, void* dst, const void* src, uint64_t bytes) {
     return guard([&] {
         ctx_lock g(c);
         if (bytes == 0) return;
+        host_pin pin_src(src, bytes), pin_dst(dst, bytes);  // large pageable host sides only
         AKB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
         AKB_CUDA(cudaStreamSynchronize(c->stream));
     });
