@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2507_16710_b200 as ak
 log2n = int(sys.argv[1]) if len(sys.argv) > 1 else 28
-dt = np.float32 if (len(sys.argv) > 2 and sys.argv[2] == "f32") else np.int64
+dt = {"f32": np.float32, "f64": np.float64}.get(sys.argv[2] if len(sys.argv) > 2 else "", np.int64)
 n = 1 << log2n
 ex = ak.ExecBackend(0)
 x = torch.from_numpy(ak.bench_keys(42, 0, n, dt)).cuda()
