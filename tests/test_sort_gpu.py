@@ -196,3 +196,29 @@ def test_sortperm_composite_msd_sizes_int32(ak, ex, dev, desc):
     want = np.argsort(-x.astype(np.int64) if desc else x, kind="stable")
     p = ak.sortperm(torch.from_numpy(x).to(dev), ex=ex, cmp="greater" if desc else None, index_dtype=torch.int32)
     assert np.array_equal(p.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n", [1_000_000, (1 << 23) + 5])
+def test_merge_sort_host_pageable_and_pinned(ak, ex, n):
+    """merge_sort_host on host arrays: a pageable numpy array (>= 32 MB is page-locked for the
+    call and released after it), an array that is already pinned (left alone), and the same
+    pageable array twice (a second registration of the same range must work)."""
+    x = ak.bench_keys(42, 1, n, np.int64)
+    want = np.sort(x)
+    for _ in range(2):
+        y = x.copy()
+        ak.merge_sort_host(y, ex)
+        assert np.array_equal(y, want)
+    pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    pinned.numpy()[:] = x
+    ak.merge_sort_host(pinned.numpy(), ex)
+    assert np.array_equal(pinned.numpy(), want)
+
+
+def test_sihsort_host_large_pageable(ak, ex):
+    """sihsort_host with pageable input and output arrays over 32 MB (both page-locked for the
+    call): equals the sorted input."""
+    n = (1 << 22) + 3
+    x = ak.bench_keys(7, 0, n, np.int64)
+    out, st = ak.sihsort_host(x, None, None, ex)
+    assert np.array_equal(out, np.sort(x))
