@@ -229,3 +229,28 @@ def test_big_range_stage_bucket_mode(ak, ex, dev, kind):
     y = x ^ (-(1 << 63))  # uint64 order as int64 order
     assert bool((y[1:] >= y[:-1]).all())
     assert _fp(x) == fp_in
+
+
+@pytest.mark.parametrize("n,desc,unsigned", [
+    ((1 << 28) + (1 << 23) - 7, False, False),   # just under the big-range threshold: 4608-key stage or host plan
+    ((1 << 28) + (1 << 23) + 9, True, False),    # just over: big-range stage, descending
+    ((1 << 29) + 3, True, True),                 # 2^29 uint64 descending: pairs of buckets per range
+])
+def test_plan_boundaries(ak, ex, dev, n, desc, unsigned):
+    """Sizes at the device plan's stage boundaries, both directions, signed and unsigned keys;
+    checked on the device (order + multiset fingerprint)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(n)
+    x = torch.randint(-(1 << 62), 1 << 62, (n,), dtype=torch.int64, device=dev, generator=g) * 2 + 1
+    fp_in = _fp(x)
+    s = torch.empty_like(x)
+    if unsigned:
+        ak.merge_sort(x.view(torch.uint64), s.view(torch.uint64), ex, cmp="greater" if desc else None)
+        y = x ^ (-(1 << 63))
+    else:
+        ak.merge_sort(x, s, ex, cmp="greater" if desc else None)
+        y = x
+    del s
+    ok = bool((y[1:] <= y[:-1]).all()) if desc else bool((y[1:] >= y[:-1]).all())
+    assert ok
+    assert _fp(x) == fp_in
