@@ -32,6 +32,9 @@ constexpr int JOINT_BINS = 1 << JOINT_BITS;
 constexpr int JH_BLOCK = 1024;
 constexpr int JH_PARTS = 4;
 constexpr std::uint32_t JH_FLUSH = 0x4000;  // u16 half-counter spill threshold
+#ifndef AKB_JH_KEYS_LOG
+#define AKB_JH_KEYS_LOG 17
+#endif
 #ifndef AKB_JH_UNROLL
 #define AKB_JH_UNROLL 8  // r02: 2 / 4 / 8 / 16 -> 0.394 / 0.355 / 0.344 / 0.344 ms at 2^28
 #endif
@@ -515,11 +518,15 @@ void msd_hist(ak_ctx* c, const T* kin, std::uint64_t n, bool desc, std::uint64_t
     smem_attr(c, hist_joint_kernel<T, true>, smem);
     smem_attr(c, hist_joint_kernel<T, false>, smem);
     AKB_CUDA(cudaMemsetAsync(g_joint, 0, JOINT_BINS * sizeof(std::uint64_t), c->stream));
+    // every CTA flushes its whole 65536-bin table into the global one: at small n fewer,
+    // fatter CTAs (one per 2^JH_KEYS_LOG keys, at least 16)
+    const unsigned grid = static_cast<unsigned>(std::max<std::uint64_t>(
+        16, std::min<std::uint64_t>(static_cast<std::uint64_t>(c->sm_count), n >> AKB_JH_KEYS_LOG)));
     const int tok = ctx_prof_begin(c, KF_HIST);
     if (digit5)
-        hist_joint_kernel<T, true><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
+        hist_joint_kernel<T, true><<<grid, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
     else
-        hist_joint_kernel<T, false><<<c->sm_count, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
+        hist_joint_kernel<T, false><<<grid, JH_BLOCK, smem, c->stream>>>(kin, n, desc ? 1 : 0, g_hist, g_joint);
     AKB_CUDA(cudaGetLastError());
     ctx_prof_end(c, tok);
     msd_joint_scan(c, g_joint, g_hist);

@@ -2310,7 +2310,9 @@ void launch_local_big(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts,
     c->kernel_launches += 1;
 }
 
-constexpr std::uint64_t SMALL_DEVICE_MAX = std::uint64_t(1) << 21;  // device-planned path up to here
+// device-planned one-level path up to here: its 8-bit buckets must fit a 4608-key CTA (uniform
+// keys: ~n / 256 + 4 sigma), so at 2^21 it was always rejected after its round trip (r02)
+constexpr std::uint64_t SMALL_DEVICE_MAX = std::uint64_t(1) << 20;
 
 // Small keys-only 64-bit integer sorts with NO host round trip before the last kernel: the top
 // three digits' histograms -> device plan (small_plan_kernel) -> one unstable partition pass
@@ -2422,6 +2424,10 @@ __global__ void two_level_plan_kernel(const std::uint64_t* __restrict__ maxslot,
 // then ONE synchronisation reading {plan, oversized-range count}. Returns false when the plan
 // was rejected (skewed keys): nothing was written, and the histograms in g_hist / msdbuf are
 // those the host plan starts from.
+#ifndef AKB_TWO_LEVEL_MIN_LOG
+#define AKB_TWO_LEVEL_MIN_LOG 20  // r02: 2^22 / 2^23 int64 0.241 / 0.314 -> 0.191 / 0.252 ms (was 24)
+#endif
+
 template <typename T>
 bool two_level_device(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t n, bool desc, std::uint64_t* g_hist,
                       std::uint64_t* msdbuf) {
@@ -2473,12 +2479,14 @@ bool hybrid_sort_keys_impl(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint6
     // two MSD levels planned on the device (the common case of 2^24 .. ~2^30 keys); a rejected
     // plan leaves the histograms for the host plan below
     bool hist_ready = false;
-    if (env < 0 && msd_env() != 0 && n >= (std::uint64_t(1) << 24) &&
+    if (env < 0 && msd_env() != 0 && n >= (std::uint64_t(1) << AKB_TWO_LEVEL_MIN_LOG) &&
         n <= (std::uint64_t(1) << 30) + (std::uint64_t(1) << 26) &&
         ((reinterpret_cast<std::uintptr_t>(kin) | reinterpret_cast<std::uintptr_t>(kalt) |
           reinterpret_cast<std::uintptr_t>(kout)) & 15) == 0) {
         if (two_level_device<T>(c, kin, kout, kalt, n, desc, g_hist, ctx_msd(c))) return true;
-        hist_ready = true;
+        // the host plan below reuses the joint read where it would have made it itself
+        // (n >= 2^24); smaller sorts plan from their own top-three-digit histogram
+        hist_ready = n >= (std::uint64_t(1) << 24);
     }
     std::uint64_t* g_offs = g_hist + PASSES * RADIX;
     std::uint32_t* counters = reinterpret_cast<std::uint32_t*>(g_offs + PASSES * RADIX);
