@@ -133,11 +133,12 @@ def test_msd_path_uint64_out_of_place(ak, ex, dev):
     assert np.array_equal(y.cpu().numpy().view(np.uint64), np.sort(x)[::-1])
 
 
-@pytest.mark.parametrize("n", [50_000, 1_000_000, 2_000_000])
+@pytest.mark.parametrize("n", [50_000, 1_000_000, 1 << 20, 2_000_000])
 def test_small_sort_graph_replays(ak, ex, dev, n):
-    """Small keys-only sorts are replayed as a CUDA graph once the same buffers come back: every
-    replay recomputes the plan from the new data (uniform, skewed, narrow, all-equal inputs
-    alternate through the same buffers) and equals np.sort."""
+    """Small keys-only sorts (n <= 2^20) are replayed as a CUDA graph once the same buffers come
+    back: every replay recomputes the plan from the new data (uniform, skewed, narrow, all-equal
+    inputs alternate through the same buffers) and equals np.sort. 2e6 keys take the
+    device-planned two-level path with the same alternation (plans rejected for skewed data)."""
     rng = np.random.default_rng(n)
     w = torch.empty(n, dtype=torch.int64, device=dev)
     s = torch.empty_like(w)
