@@ -183,10 +183,15 @@ __global__ void __launch_bounds__(1024) joint_scan_b_kernel(std::uint64_t* __res
     const std::uint64_t c = cur16[i] + s_off;
     cur16[i] = c;
     if ((i & 0xff) == 0) cur8[i >> 8] = c;
-    if (blockIdx.x == 0 && t < 256) {
+    if (blockIdx.x == 0) {  // column sums: 4 threads per column, 16 partials each (no long serial chain)
+        const int col = t & 255, q = t >> 8;
         std::uint64_t x = 0;
-        for (int k = 0; k < JS_CTAS; ++k) x += colpart[k * 256 + t];
-        g_hist[6 * 256 + t] += x;
+#pragma unroll
+        for (int k = q; k < JS_CTAS; k += 4) x += colpart[k * 256 + col];
+        __shared__ std::uint64_t s_col[3][256];
+        if (q) s_col[q - 1][col] = x;
+        __syncthreads();
+        if (q == 0) g_hist[6 * 256 + col] += x + s_col[0][col] + s_col[1][col] + s_col[2][col];
     }
 }
 
