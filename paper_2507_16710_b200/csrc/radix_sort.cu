@@ -2313,6 +2313,9 @@ void launch_local_big(ak_ctx* c, const T* G, T* kout, const std::uint64_t* cuts,
 // device-planned one-level path up to here: its 8-bit buckets must fit a 4608-key CTA (uniform
 // keys: ~n / 256 + 4 sigma), so at 2^21 it was always rejected after its round trip (r02)
 constexpr std::uint64_t SMALL_DEVICE_MAX = std::uint64_t(1) << 20;
+#ifndef AKB_SMALL_HIST_KEYS
+#define AKB_SMALL_HIST_KEYS 4096  // keys per histogram CTA of a small sort (r02: 16384 / 8192 / 4096 / 2048 -> 55 / 53 / 52 / 54 us per 1e6 sort)
+#endif
 
 // Small keys-only 64-bit integer sorts with NO host round trip before the last kernel: the top
 // three digits' histograms -> device plan (small_plan_kernel) -> one unstable partition pass
@@ -2336,10 +2339,11 @@ bool small_sort_device(ak_ctx* c, const T* kin, T* kout, T* kalt, std::uint64_t 
     std::uint64_t* big = cuts + J + 2;
     std::uint64_t* redo = big + J + 1;
     auto* h = static_cast<std::uint64_t*>(ctx_pinned(c, 2 * sizeof(std::uint64_t)));
-    // few, fat histogram CTAs: each flushes 3 x 256 global atomics, which dominate at small n
+    // one histogram CTA per 4096 keys (at most 4 per SM): each flushes 3 x 256 global atomics,
+    // so fewer, fatter CTAs flush less but read with less parallelism
     const unsigned hist_grid = static_cast<unsigned>(
         std::max<std::uint64_t>(1, std::min<std::uint64_t>(static_cast<std::uint64_t>(c->sm_count) * 4,
-                                                            ceil_div(n, 256 * 64))));
+                                                            ceil_div(n, AKB_SMALL_HIST_KEYS))));
     auto enqueue = [&] {
         AKB_CUDA(cudaMemsetAsync(g_hist + (PASSES - 3) * RADIX, 0, 3 * RADIX * sizeof(std::uint64_t), c->stream));
         const int tok = ctx_prof_begin(c, KF_HIST);
