@@ -121,14 +121,19 @@ void merge_sort_impl(ak_ctx* c, T* data, std::uint64_t n, T* scratch, std::uint6
     akb::ctx_finish(c);
 }
 
-// A caller's large pageable host array is page-locked for the duration of one call (its copies
-// then run at the link's DMA rate instead of through the driver's staging buffers); arrays
-// that are already pinned or registered, and ones under 32 MB (registering costs ~1 ms),
-// are left alone. merge_sort_host of 2^24 int64: 18.7 -> 11.0 ms, 2^27: 147 -> 79 ms.
+// A caller's large pageable host array is page-locked for the duration of one in-place host
+// sort (its two copies then run at the link's DMA rate instead of through the driver's
+// staging buffers); arrays that are already pinned or registered, and ones under 32 MB
+// (registering costs ~1 ms), are left alone. merge_sort_host of 2^24 int64: 18.7 -> 11.0 ms,
+// 2^27: 147 -> 79 ms. Not used for one-way copies: the C++ headers' staging (ak_memcpy) of
+// fresh 512 MB vectors got slower with it (ak_bench sort-weak 2^26 host path 545 -> 725 ms).
+#ifndef AKB_HOST_PIN_MIN_MB
+#define AKB_HOST_PIN_MIN_MB 32
+#endif
 struct host_pin {
     void* p = nullptr;
     host_pin(const void* ptr, std::size_t bytes) {
-        if (!ptr || bytes < (std::size_t(32) << 20)) return;
+        if (!ptr || bytes < (std::size_t(AKB_HOST_PIN_MIN_MB) << 20)) return;
         cudaPointerAttributes a{};
         if (cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type != cudaMemoryTypeUnregistered) return;
         (void)cudaGetLastError();
@@ -313,7 +318,6 @@ void sihsort_host_impl(ak_ctx* c, ak_comm* comm, const T* h_in, std::uint64_t n,
     need(out_count != nullptr, "sihsort: null out_count");
     need(n == 0 || h_in, "sihsort: null input");
     need(cap == 0 || h_out, "sihsort: null output");
-    host_pin pin_in(h_in, n * sizeof(T)), pin_out(h_out, cap * sizeof(T));
     T* d = static_cast<T*>(akb::ctx_stage(c, (n + cap + 1) * sizeof(T)));
     T* d_in = d;
     T* d_out = d + n;
@@ -685,6 +689,7 @@ int ak_ctx_destroy(ak_ctx* c) {
         if (c->stage) cudaFree(c->stage);
         if (c->work) cudaFree(c->work);
         if (c->pinned) cudaFreeHost(c->pinned);
+        for (auto& b : c->free_blocks) cudaFree(b.second);
         for (auto& t : c->pending) {
             cudaEventDestroy(t.a);
             cudaEventDestroy(t.b);
@@ -752,25 +757,75 @@ int ak_ctx_reset_kernel_time(ak_ctx* c) {
 uint64_t ak_ctx_kernel_launches(const ak_ctx* c) { return c ? c->kernel_launches : 0; }
 void* ak_ctx_stream(const ak_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
+// ak_malloc / ak_free keep freed blocks on the ctx and hand them out again (smallest block
+// that fits and is at most twice the request), so a caller that stages through fresh device
+// buffers on every call -- the C++ headers with host spans, ak_bench without
+// --device-resident -- does not pay a GiB-sized cudaMalloc / cudaFree per call. At most
+// 1/4 of the device memory (or 16 GiB) is held; ak_ctx_destroy releases everything.
+namespace {
+std::size_t free_cap(ak_ctx* c) {
+    std::size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        (void)cudaGetLastError();
+        tot = std::size_t(64) << 30;
+    }
+    (void)c;
+    return std::min<std::size_t>(tot / 4, std::size_t(16) << 30);
+}
+}  // namespace
+
 int ak_malloc(ak_ctx* c, uint64_t bytes, void** out) {
     return guard([&] {
         ctx_lock g(c);
         need(out != nullptr, "ak_malloc: null out");
-        AKB_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+        const std::size_t want = bytes ? bytes : 1;
+        std::size_t best = c->free_blocks.size();
+        for (std::size_t i = 0; i < c->free_blocks.size(); ++i) {
+            const std::size_t sz = c->free_blocks[i].first;
+            if (sz >= want && sz <= 2 * want && (best == c->free_blocks.size() || sz < c->free_blocks[best].first))
+                best = i;
+        }
+        if (best < c->free_blocks.size()) {
+            *out = c->free_blocks[best].second;
+            c->live_blocks.emplace_back(*out, c->free_blocks[best].first);
+            c->free_bytes -= c->free_blocks[best].first;
+            c->free_blocks.erase(c->free_blocks.begin() + static_cast<std::ptrdiff_t>(best));
+            return;
+        }
+        AKB_CUDA(cudaMalloc(out, want));
+        c->live_blocks.emplace_back(*out, want);
     });
 }
 int ak_free(ak_ctx* c, void* p) {
     return guard([&] {
         ctx_lock g(c);
-        AKB_CUDA(cudaStreamSynchronize(c->stream));
-        AKB_CUDA(cudaFree(p));
+        if (!p) return;
+        AKB_CUDA(cudaStreamSynchronize(c->stream));  // the block may still be read by queued work
+        std::size_t sz = 0;
+        for (std::size_t i = 0; i < c->live_blocks.size(); ++i)
+            if (c->live_blocks[i].first == p) {
+                sz = c->live_blocks[i].second;
+                c->live_blocks.erase(c->live_blocks.begin() + static_cast<std::ptrdiff_t>(i));
+                break;
+            }
+        if (sz == 0) {  // not ours (or unknown): release it
+            AKB_CUDA(cudaFree(p));
+            return;
+        }
+        c->free_blocks.emplace_back(sz, p);
+        c->free_bytes += sz;
+        const std::size_t cap = free_cap(c);
+        while (c->free_bytes > cap && !c->free_blocks.empty()) {  // oldest first
+            AKB_CUDA(cudaFree(c->free_blocks.front().second));
+            c->free_bytes -= c->free_blocks.front().first;
+            c->free_blocks.erase(c->free_blocks.begin());
+        }
     });
 }
 int ak_memcpy(ak_ctx* c, void* dst, const void* src, uint64_t bytes) {
     return guard([&] {
         ctx_lock g(c);
         if (bytes == 0) return;
-        host_pin pin_src(src, bytes), pin_dst(dst, bytes);  // large pageable host sides only
         AKB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
         AKB_CUDA(cudaStreamSynchronize(c->stream));
     });

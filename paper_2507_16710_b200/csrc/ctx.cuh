@@ -67,6 +67,11 @@ struct ak_ctx {
     std::size_t stage_bytes = 0;
 
     // pinned host staging for small device->host reads
+    // blocks returned by ak_free, kept for reuse by ak_malloc (the C++ headers stage host
+    // spans through per-call device buffers): size -> pointer, at most free_cap bytes held
+    std::vector<std::pair<std::size_t, void*>> free_blocks;
+    std::size_t free_bytes = 0;
+    std::vector<std::pair<void*, std::size_t>> live_blocks;  // ak_malloc'd and not yet freed
     void* pinned = nullptr;
     std::size_t pinned_bytes = 0;
 
