@@ -1834,7 +1834,6 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
     std::uint32_t phase = 0;
     const bool copy_equal = in != out;
 
-#pragma unroll 1
     // the range bounds are loaded one range ahead (one CTA per SM: a cold global load per
     // range would sit on the critical path)
     std::uint64_t nb_ = 0, ne_ = 0;
@@ -1842,6 +1841,7 @@ __global__ void __launch_bounds__(LB_BLOCK, 1)
         nb_ = cuts[blockIdx.x];
         ne_ = cuts[blockIdx.x + 1];
     }
+#pragma unroll 1
     for (std::uint32_t r = blockIdx.x; r < nr; r += gridDim.x) {
         const std::uint64_t b = nb_, e = ne_;
         if (r + gridDim.x < nr) {
